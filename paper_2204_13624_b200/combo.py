@@ -1,0 +1,403 @@
+"""ctypes bindings of libcombo_cuda.so mirroring the reference API.
+
+Reference interfaces mirrored (/root/reference/proj/include/combo):
+  solve(CellMaterials&, fbar, SolverConfig)      solver.hpp:68-69
+  CellMaterials(grid, matrix, inclusion, combo)  cell_material.hpp:22-23
+  stress_sweep / tangent_matvec                  cell_material.hpp:90-96
+  GreenOperator::project                         green.hpp:40
+  coarsen / compute_normals / laplace_weights    combo_grid.hpp:62, normals.hpp:26-61
+  generate_*                                     image.hpp:47-88
+Error codes map onto the reference exception types (errors.hpp:11-55).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+GREEN = {"continuous": 0, "rotated": 1, "staggered": 2}
+SCHEME = {"basic": 0, "newton_cg": 1}
+EVAL = {"per_cell": 0, "dfmg": 1}
+MEM_HOST, MEM_DEVICE = 0, 1
+
+_ERRORS = {
+    -1: "ConfigInvalid", -2: "InadmissibleMacroState", -3: "LoadPathFailed", -4: "SingularMatrix",
+    -5: "NonDividingFactor", -6: "BadShapeSpec", -10: "CudaError", -11: "NcclError", -12: "OutOfMemory",
+    -13: "BadArgument", -14: "BadState",
+}
+
+
+class ComboError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        self.type = _ERRORS.get(code, "Error")
+        super().__init__(f"{self.type} ({code}): {msg}")
+
+
+class Law(C.Structure):  # combo_law
+    _fields_ = [("kind", C.c_int), ("lam", C.c_double), ("mu", C.c_double), ("c6", C.c_double * 36)]
+
+
+class LamOpts(C.Structure):  # combo_laminate_opts
+    _fields_ = [("tol_abs", C.c_double), ("tol_rel", C.c_double), ("stress_floor", C.c_double),
+                ("max_iter", C.c_int), ("back_projection", C.c_int), ("c_min", C.c_double)]
+
+
+class SolverCfg(C.Structure):  # combo_solver_cfg
+    _fields_ = [("scheme", C.c_int), ("green", C.c_int), ("eval", C.c_int), ("tol_equilibrium", C.c_double),
+                ("max_outer", C.c_int), ("cg_tol", C.c_double), ("cg_max", C.c_int), ("load_steps", C.c_int),
+                ("max_bisections", C.c_int), ("threads", C.c_int), ("verbose", C.c_int),
+                ("max_ls_iterations", C.c_longlong)]
+
+
+class SweepStats(C.Structure):
+    _fields_ = [("inadmissible_cells", C.c_int64), ("laminate_failures", C.c_int64),
+                ("back_projections", C.c_int64), ("laminate_iter_max", C.c_int64)]
+
+
+class NormalStats(C.Structure):
+    _fields_ = [("composite", C.c_int64), ("degenerate_fallbacks", C.c_int64), ("too_few_fallbacks", C.c_int64)]
+
+
+def lib_path():
+    return os.path.join(_HERE, "libcombo_cuda.so")
+
+
+_D = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_U8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+_I64 = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_VP = C.c_void_p
+
+# symbol -> (restype, argtypes); every function of include/combo_cuda.h
+SIGNATURES = {
+    "combo_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "combo_ctx_destroy": (C.c_int, [_VP]),
+    "combo_last_error": (C.c_char_p, [_VP]),
+    "combo_version": (C.c_char_p, []),
+    "combo_kernel_launches": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
+    "combo_synchronize": (C.c_int, [_VP]),
+    "combo_generate": (C.c_int, [_VP, C.c_int, _I64, _D, _D, C.c_int, _VP, C.c_int]),
+    "combo_coarsen": (C.c_int, [_VP, _VP, _I64, _I64, _VP, _VP, _VP, C.c_int]),
+    "combo_laplace_weights": (C.c_int, [_VP, _VP, _I64, _D, _VP, C.c_int]),
+    "combo_normals": (C.c_int, [_VP, _VP, _I64, _D, _I64, _VP, C.c_int, C.c_int, C.c_int, _VP, _VP,
+                                C.POINTER(NormalStats), C.c_int]),
+    "combo_set_grid": (C.c_int, [_VP, _I64, _D]),
+    "combo_bind_materials": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, C.POINTER(Law), C.POINTER(Law), C.c_int,
+                                       C.POINTER(LamOpts), C.c_int]),
+    "combo_composite_cells": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
+    "combo_stress_floor": (C.c_int, [_VP, C.POINTER(C.c_double)]),
+    "combo_get_warm_starts": (C.c_int, [_VP, _VP, C.c_int]),
+    "combo_set_warm_starts": (C.c_int, [_VP, _VP, C.c_int]),
+    "combo_spectrum_bounds": (C.c_int, [_VP, _D, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "combo_stress_sweep": (C.c_int, [_VP, _VP, _VP, C.POINTER(SweepStats), C.c_int]),
+    "combo_tangent_matvec": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
+    "combo_tangent45": (C.c_int, [_VP, _VP, _VP, C.c_int]),
+    "combo_tangent45_matvec": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
+    "combo_project": (C.c_int, [_VP, C.c_int, _VP, _VP, C.c_int]),
+    "combo_fft_forward": (C.c_int, [_VP, _I64, C.c_int, _VP, _VP, C.c_int]),
+    "combo_dfmg_stress": (C.c_int, [_VP, _VP, _VP, C.POINTER(SweepStats), C.c_int]),
+    "combo_dfmg_tangent_matvec": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
+    "combo_dfmg_get_warm_starts": (C.c_int, [_VP, _VP, C.c_int]),
+    "combo_laminate_solve": (C.c_int, [_VP, _D, C.POINTER(Law), C.POINTER(Law), _D, C.c_double, _D,
+                                       C.POINTER(LamOpts), _D, _D, np.ctypeslib.ndpointer(dtype=np.int32)]),
+    "combo_solve": (C.c_int, [_VP, _D, C.POINTER(SolverCfg), _VP, _VP, _D, C.POINTER(C.c_void_p), C.c_int]),
+    "combo_report_summary": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "combo_report_step": (C.c_int, [_VP, C.c_int, _VP]),
+    "combo_report_step_history": (C.c_int, [_VP, C.c_int, _VP, _VP, _VP]),
+    "combo_report_json": (C.c_char_p, [_VP]),
+    "combo_report_free": (C.c_int, [_VP]),
+}
+
+
+def load_library(path=None):
+    """Load libcombo_cuda.so (no fallback: raises if it is missing)."""
+    global _LIB
+    if _LIB is None:
+        p = path or lib_path()
+        if not os.path.exists(p):
+            raise ComboError(-14, f"{p} missing: build it with __graft_entry__.build()")
+        L = C.CDLL(p)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return C.c_void_p(a)
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def neo_hookean(lam, mu):
+    """NeoHookeanParams given as (lambda, mu) (materials.hpp:14-21)."""
+    return Law(0, float(lam), float(mu))
+
+
+def neo_hookean_enu(e, nu):
+    """NeoHookeanParams::from_enu (materials.cpp:11-20)."""
+    return neo_hookean(e * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), e / (2.0 * (1.0 + nu)))
+
+
+def iso_mandel(lam, mu):
+    """LinearElasticParams::isotropic (materials.cpp:22-30)."""
+    c = np.zeros((6, 6))
+    c[:3, :3] = lam
+    for i in range(3):
+        c[i, i] += 2.0 * mu
+        c[i + 3, i + 3] = 2.0 * mu
+    return c
+
+
+def linear(c6):
+    law = Law(1, 0.0, 0.0)
+    for i, v in enumerate(np.asarray(c6, dtype=np.float64).ravel()):
+        law.c6[i] = v
+    return law
+
+
+@dataclass
+class LaminateOptions:  # laminate.hpp:72-79
+    tol_abs: float = 0.0
+    tol_rel: float = 1e-10
+    stress_floor: float = 0.0
+    max_iter: int = 50
+    back_projection: bool = True
+    c_min: float = 0.0
+
+    def c(self):
+        return LamOpts(self.tol_abs, self.tol_rel, self.stress_floor, self.max_iter, int(self.back_projection),
+                       self.c_min)
+
+
+@dataclass
+class SolverConfig:  # solver.hpp:18-32
+    scheme: str = "newton_cg"
+    green: str = "rotated"
+    eval: str = "per_cell"
+    tol_equilibrium: float = 1e-8
+    max_outer: int = 200
+    cg_tol: float = 1e-2
+    cg_max: int = 2000
+    load_steps: int = 1
+    max_bisections: int = 5
+    verbose: bool = False
+    max_ls_iterations: int = 0
+
+    def c(self):
+        return SolverCfg(SCHEME[self.scheme], GREEN[self.green], EVAL[self.eval], self.tol_equilibrium,
+                         self.max_outer, self.cg_tol, self.cg_max, self.load_steps, self.max_bisections, 0,
+                         int(self.verbose), self.max_ls_iterations)
+
+
+def _i64(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int64))
+
+
+def _f64(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+class Context:
+    """One device + stream (combo_ctx)."""
+
+    def __init__(self, device=0):
+        self.L = load_library()
+        h = C.c_void_p()
+        self._check(self.L.combo_ctx_create(int(device), C.byref(h)), ctx=None)
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.combo_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, ctx="self"):
+        if rc != 0:
+            msg = self.L.combo_last_error(self.h if ctx == "self" else None)
+            raise ComboError(rc, msg.decode() if msg else "")
+
+    @property
+    def kernel_launches(self):
+        v = C.c_int64()
+        self._check(self.L.combo_kernel_launches(self.h, C.byref(v)))
+        return int(v.value)
+
+    # ------------------------------------------------------------ images
+    def generate(self, shape, dims, lengths=(1.0, 1.0, 1.0), *params):
+        ids = {"sphere": 0, "octahedron": 1, "slab": 5, "rsa_spheres": 10, "rsa_fibers_z": 11,
+               "boolean_ellipsoids": 12}
+        out = np.zeros(int(np.prod(dims)), dtype=np.uint8)
+        p = _f64(list(params) + [0.0] * (8 - len(params)))
+        self._check(self.L.combo_generate(self.h, ids[shape], _i64(dims), _f64(lengths), p, len(params),
+                                          _ptr(out), MEM_HOST))
+        return out.reshape(tuple(dims))
+
+    def coarsen(self, img, factors):
+        """coarsen (combo_grid.cpp:28-71) -> kind, c_plus, count_plus"""
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        dims = _i64(img.shape)
+        f = _i64(factors)
+        nb = int(np.prod(dims // np.maximum(f, 1)))
+        kind = np.zeros(nb, np.uint8)
+        cp = np.zeros(nb)
+        cnt = np.zeros(nb, np.int64)
+        self._check(self.L.combo_coarsen(self.h, _ptr(img), dims, f, _ptr(kind), _ptr(cp), _ptr(cnt), MEM_HOST))
+        return kind, cp, cnt
+
+    def laplace_weights(self, img, lengths=(1.0, 1.0, 1.0)):
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        w = np.zeros(img.size)
+        self._check(self.L.combo_laplace_weights(self.h, _ptr(img), _i64(img.shape), _f64(lengths), _ptr(w),
+                                                 MEM_HOST))
+        return w.reshape(img.shape)
+
+    def compute_normals(self, img, factors, kind, lengths=(1.0, 1.0, 1.0), method="second_moment",
+                        centering="weighted_centroid", min_interface_voxels=3):
+        """compute_normals (normals.cpp:211-256) -> normals (nb,3), flags, stats"""
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        kind = np.ascontiguousarray(kind, dtype=np.uint8)
+        nb = kind.size
+        n3 = np.zeros(3 * nb)
+        flags = np.zeros(nb, np.uint8)
+        st = NormalStats()
+        m = {"barycenter": 0, "second_moment": 1}[method]
+        cen = {"weighted_centroid": 0, "boxel_center": 1}[centering]
+        self._check(self.L.combo_normals(self.h, _ptr(img), _i64(img.shape), _f64(lengths), _i64(factors),
+                                         _ptr(kind), m, cen, int(min_interface_voxels), _ptr(n3), _ptr(flags),
+                                         C.byref(st), MEM_HOST))
+        return n3.reshape(nb, 3), flags, (st.composite, st.degenerate_fallbacks, st.too_few_fallbacks)
+
+    # --------------------------------------------------------- operators
+    def set_grid(self, dims, lengths=(1.0, 1.0, 1.0)):
+        self._check(self.L.combo_set_grid(self.h, _i64(dims), _f64(lengths)))
+
+    def project(self, field, kind="rotated", dims=None, lengths=(1.0, 1.0, 1.0)):
+        """GreenOperator::project (green.cpp:133-151) on a 9 x N field"""
+        if dims is not None:
+            self.set_grid(dims, lengths)
+        f = _f64(field).ravel()
+        out = np.zeros_like(f)
+        self._check(self.L.combo_project(self.h, GREEN[kind] if isinstance(kind, str) else int(kind), _ptr(f),
+                                         _ptr(out), MEM_HOST))
+        return out
+
+    def fft_forward(self, dims, field):
+        n1, n2, n3 = dims
+        ncomp = int(np.asarray(field).size // (n1 * n2 * n3))
+        out = np.zeros(2 * ncomp * n1 * n2 * (n3 // 2 + 1))
+        self._check(self.L.combo_fft_forward(self.h, _i64(dims), ncomp, _ptr(_f64(field).ravel()), _ptr(out),
+                                             MEM_HOST))
+        return out.view(np.complex128).reshape(ncomp, n1, n2, n3 // 2 + 1)
+
+    def laminate_solve(self, fbox, plus, minus, normal, c_plus, a0=(0, 0, 0), opts=None):
+        opts = opts or LaminateOptions()
+        p = np.zeros(9)
+        a = np.zeros(3)
+        ist = np.zeros(4, np.int32)
+        oc = opts.c()
+        self._check(self.L.combo_laminate_solve(self.h, _f64(np.asarray(fbox).ravel()), C.byref(plus),
+                                                C.byref(minus), _f64(normal), float(c_plus), _f64(a0),
+                                                C.byref(oc), p, a, ist))
+        return dict(p_box=p.reshape(3, 3), a=a, converged=bool(ist[0]), iterations=int(ist[1]),
+                    back_projections=int(ist[2]))
+
+
+class CellMaterials:
+    """CellMaterials (cell_material.hpp:19-74) bound on the device."""
+
+    def __init__(self, ctx, dims, kind, c_plus, normal, matrix, inclusion, combo=True, opts=None,
+                 lengths=(1.0, 1.0, 1.0)):
+        self.ctx = ctx
+        self.dims = tuple(int(d) for d in dims)
+        self.lengths = tuple(float(x) for x in lengths)
+        self.n = int(np.prod(self.dims))
+        kind = np.ascontiguousarray(kind, dtype=np.uint8).ravel()
+        cp = _f64(c_plus).ravel()
+        nrm = None if normal is None else _f64(normal).ravel()
+        oc = (opts or LaminateOptions()).c()
+        ctx._check(ctx.L.combo_bind_materials(ctx.h, _i64(self.dims), _f64(self.lengths), _ptr(kind), _ptr(cp),
+                                              _ptr(nrm), C.byref(matrix), C.byref(inclusion), int(combo),
+                                              C.byref(oc), MEM_HOST))
+
+    @property
+    def composites(self):
+        v = C.c_int64()
+        self.ctx._check(self.ctx.L.combo_composite_cells(self.ctx.h, C.byref(v)))
+        return int(v.value)
+
+    @property
+    def stress_floor(self):
+        v = C.c_double()
+        self.ctx._check(self.ctx.L.combo_stress_floor(self.ctx.h, C.byref(v)))
+        return float(v.value)
+
+    def warm(self, value=None):
+        buf = np.zeros(3 * self.composites)
+        if value is None:
+            self.ctx._check(self.ctx.L.combo_get_warm_starts(self.ctx.h, _ptr(buf), MEM_HOST))
+            return buf.reshape(-1, 3)
+        buf[:] = np.asarray(value, dtype=np.float64).ravel()
+        self.ctx._check(self.ctx.L.combo_set_warm_starts(self.ctx.h, _ptr(buf), MEM_HOST))
+
+    def stress_sweep(self, F):
+        F = _f64(F).ravel()
+        P = np.zeros_like(F)
+        st = SweepStats()
+        self.ctx._check(self.ctx.L.combo_stress_sweep(self.ctx.h, _ptr(F), _ptr(P), C.byref(st), MEM_HOST))
+        return P, (st.inadmissible_cells, st.laminate_failures, st.back_projections, st.laminate_iter_max)
+
+    def tangent_matvec(self, F, x):
+        y = np.zeros(9 * self.n)
+        self.ctx._check(self.ctx.L.combo_tangent_matvec(self.ctx.h, _ptr(_f64(F).ravel()), _ptr(_f64(x).ravel()),
+                                                        _ptr(y), MEM_HOST))
+        return y
+
+    def tangent45(self, F):
+        t = np.zeros(45 * self.n)
+        self.ctx._check(self.ctx.L.combo_tangent45(self.ctx.h, _ptr(_f64(F).ravel()), _ptr(t), MEM_HOST))
+        return t
+
+    def dfmg_stress(self, F):
+        F = _f64(F).ravel()
+        P = np.zeros_like(F)
+        st = SweepStats()
+        self.ctx._check(self.ctx.L.combo_dfmg_stress(self.ctx.h, _ptr(F), _ptr(P), C.byref(st), MEM_HOST))
+        return P, (st.inadmissible_cells, st.laminate_failures, st.back_projections, st.laminate_iter_max)
+
+    def dfmg_tangent_matvec(self, F, x):
+        y = np.zeros(9 * self.n)
+        self.ctx._check(self.ctx.L.combo_dfmg_tangent_matvec(self.ctx.h, _ptr(_f64(F).ravel()),
+                                                             _ptr(_f64(x).ravel()), _ptr(y), MEM_HOST))
+        return y
+
+    def solve(self, fbar, cfg=None, want_fields=True, **kw):
+        """solve (solver.cpp:286-346) -> dict(f, p, pbar, report)"""
+        cfg = cfg or SolverConfig(**kw)
+        F = np.zeros(9 * self.n) if want_fields else None
+        P = np.zeros(9 * self.n) if want_fields else None
+        pbar = np.zeros(9)
+        rep = C.c_void_p()
+        cc = cfg.c()
+        L = self.ctx.L
+        self.ctx._check(L.combo_solve(self.ctx.h, _f64(np.asarray(fbar).ravel()), C.byref(cc), _ptr(F), _ptr(P),
+                                      pbar, C.byref(rep), MEM_HOST))
+        report = json.loads(L.combo_report_json(rep).decode())
+        L.combo_report_free(rep)
+        return dict(f=F, p=P, pbar=pbar.reshape(3, 3), report=report)

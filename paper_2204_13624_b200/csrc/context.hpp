@@ -1,0 +1,206 @@
+// Host-side context of the B200 ComBo engine (one device, one stream).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/combo_cuda.h"
+#include "fft.cuh"
+#include "kernels.cuh"
+#include "material.cuh"
+
+namespace combo_host {
+
+struct ComboError : std::exception {
+  int code;
+  std::string msg;
+  ComboError(int c, std::string m) : code(c), msg(std::move(m)) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+
+#define COMBO_CK(x)                                                                                     \
+  do {                                                                                                  \
+    cudaError_t e_ = (x);                                                                               \
+    if (e_ != cudaSuccess)                                                                              \
+      throw ::combo_host::ComboError(e_ == cudaErrorMemoryAllocation ? COMBO_ERR_OOM : COMBO_ERR_CUDA, \
+                                     std::string(#x) + ": " + cudaGetErrorString(e_));                  \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    COMBO_CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+};
+
+struct AxisPlan {
+  int n = 1;
+  std::vector<int> rad;
+  DBuf<double2> tw;
+  combo_dev::Axis view() const {
+    combo_dev::Axis a{};
+    a.n = n;
+    a.nrad = int(rad.size());
+    for (size_t i = 0; i < rad.size(); ++i) a.rad[i] = rad[i];
+    a.tw = tw.p;
+    return a;
+  }
+};
+
+struct GreenPlan {
+  int kind = -1;
+  DBuf<double2> fwd[3], avg[3];
+  DBuf<double> xi[3];
+};
+
+// FFT + Gamma plan for one grid
+struct FftPlan {
+  std::array<int64_t, 3> dims{0, 0, 0};
+  std::array<double, 3> lengths{1, 1, 1};
+  int64_t n3c = 0, n3p = 0;
+  AxisPlan ax[3];
+  GreenPlan green[3];
+  int zL = 1, zls = 1, zT = 32;  // z pass: lines per block, line stride, threads
+  int yW = 8, yT = 32;           // y pass tile width, threads
+  int xW = 8, xT = 32;           // x pass tile width (3 components per tile)
+  size_t zsmem = 0, ysmem = 0, xsmem = 0;
+  DBuf<double2> spec;
+  combo_dev::SpecView sv() const {
+    combo_dev::SpecView s;
+    s.spec = spec.p;
+    s.n1 = dims[0];
+    s.n2 = dims[1];
+    s.n3 = dims[2];
+    s.n3c = n3c;
+    s.n3p = n3p;
+    return s;
+  }
+};
+
+struct StepRec {
+  double t_start = 0, t_end = 0;
+  double fbar[9] = {0};
+  bool converged = false;
+  int outer_iters = 0;
+  std::vector<double> residuals;
+  std::vector<int> cg_iters;
+  std::vector<std::array<double, 9>> pbar_history;
+  int cg_breakdowns = 0;
+  int line_search_cuts = 0;
+  combo_sweep_stats sweep{0, 0, 0, 0};
+  double seconds = 0;
+  int64_t ls_basic = 0, ls_residual = 0, ls_cg = 0, ls_trial = 0;
+};
+
+}  // namespace combo_host
+
+struct combo_report {
+  std::vector<combo_host::StepRec> steps;
+  bool success = false;
+  std::string error;
+  int bisections = 0;
+  double alpha = 0;
+  double seconds_total = 0;
+  int64_t ls_total = 0;
+  std::string json;
+};
+
+struct combo_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // grid (set by combo_set_grid / combo_bind_materials)
+  bool has_grid = false;
+  std::array<int64_t, 3> dims{0, 0, 0};
+  std::array<double, 3> lengths{1, 1, 1};
+  int64_t N = 0;
+  std::unique_ptr<combo_host::FftPlan> plan;
+
+  // materials (combo_bind_materials)
+  bool bound = false;
+  combo_law law_m{}, law_i{};
+  combo_laminate_opts lam{};
+  double stress_floor = 1e-300;
+  combo_host::DBuf<int32_t> cid;
+  combo_host::DBuf<double> nrm, cp, cm, warm;
+  int64_t ncomp = 0;
+  combo_dev::MatParams mp{};
+  combo_host::DBuf<double> a9;  // linear-law 9x9 tangents (device)
+  combo_host::DBuf<double> dfmg_warm;  // [3][8N] per doubly-fine cell
+
+  // scratch
+  combo_host::DBuf<double> partials;   // per-block partial sums
+  combo_host::DBuf<double> dres;       // reduced scalars (64 slots)
+  combo_host::DBuf<combo_dev::Stats> dstats;
+  double* hres = nullptr;              // pinned mirror of dres + stats
+  combo_host::DBuf<double> scratch[4];  // operator-level staging (9N each)
+
+  // CUDA-event profiling of every kernel launch (combo_profile_*)
+  struct ProfRec {
+    int tag;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  std::string prof_json;
+
+  combo_dev::CellData cell_data() const {
+    combo_dev::CellData c;
+    c.cid = cid.p;
+    c.nrm = nrm.p;
+    c.cp = cp.p;
+    c.cm = cm.p;
+    c.warm = warm.p;
+    c.ncomp = ncomp;
+    return c;
+  }
+};
+
+namespace combo_host {
+// engine.cu
+void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths);
+int ew_grid(int64_t n);
+void ensure_scratch(combo_ctx* c);
+void reduce_partials(combo_ctx* c, int64_t nblocks, int nred, int slot);
+void fetch_results(combo_ctx* c);  // dres + stats -> hres (sync)
+combo_dev::LawP law_params(const combo_law& L, double* dev_a9);
+
+// kernel tags for the profiler
+enum ProfTag {
+  kTagSweep, kTagMatvec, kTagZfwd, kTagYfwd, kTagXGamma, kTagYinv, kTagZinv, kTagCgUpdate, kTagTrial,
+  kTagMaterialize, kTagReduce, kTagOther, kNumTags
+};
+// RAII: records CUDA events around the launches in its scope when enabled
+struct ProfScope {
+  combo_ctx* c;
+  int idx = -1;
+  ProfScope(combo_ctx* ctx, int tag, double bytes);
+  ~ProfScope();
+};
+}  // namespace combo_host

@@ -1,0 +1,1419 @@
+// B200 ComBo engine: FFT/Gamma plans, fused projection pipeline, stress /
+// tangent sweeps and the Lippmann-Schwinger solver driver (basic fixed point
+// and Newton-CG with line search and load-step bisection).
+//
+// Host control flow restates /root/reference/proj/src/solver.cpp:124-346
+// line by line; every field-sized operation is a kernel of this library and
+// only scalars (sums, stats) cross PCIe per iteration.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+#include <type_traits>
+
+#include "context.hpp"
+
+using namespace combo_dev;
+
+namespace combo_host {
+
+// ------------------------------------------------------------------ plans
+namespace {
+constexpr long double kPiL = 3.141592653589793238462643383279502884L;
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+std::vector<int> factor_radices(int n) {
+  std::vector<int> r;
+  int m = n;
+  while (m % 8 == 0) {
+    r.push_back(8);
+    m /= 8;
+  }
+  while (m % 4 == 0) {
+    r.push_back(4);
+    m /= 4;
+  }
+  while (m % 2 == 0) {
+    r.push_back(2);
+    m /= 2;
+  }
+  for (int p = 3; m > 1; p += 2)
+    while (m % p == 0) {
+      if (p > 61) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "FFT: prime factor > 61 unsupported");
+      r.push_back(p);
+      m /= p;
+    }
+  if (r.size() > size_t(kMaxRad)) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "FFT: too many radix stages");
+  return r;
+}
+
+void build_axis(AxisPlan& a, int n) {
+  a.n = n;
+  a.rad = factor_radices(n);
+  std::vector<double2> tw(size_t(std::max(n, 1)));
+  for (int k = 0; k < n; ++k) {
+    const long double ph = -2.0L * kPiL * (long double)k / (long double)n;
+    tw[size_t(k)] = make_double2(double(cosl(ph)), double(sinl(ph)));
+  }
+  a.tw.alloc(tw.size());
+  COMBO_CK(cudaMemcpy(a.tw.p, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+}
+
+// one radix-8 butterfly (8 complex values) per thread per stage
+int pick_threads(int64_t tile) {
+  const int64_t t = ((tile + kElems - 1) / kElems + 31) / 32 * 32;
+  if (t > kMaxFftThreads) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "FFT tile too large");
+  return int(std::max<int64_t>(t, 32));
+}
+
+// green.cpp:16-57 (identical double arithmetic to the reference)
+void build_green(GreenPlan& g, int kind, const std::array<int64_t, 3>& dims,
+                 const std::array<double, 3>& lengths) {
+  g.kind = kind;
+  for (int a = 0; a < 3; ++a) {
+    const int64_t n = dims[a];
+    const double h = lengths[a] / double(n);
+    const double l = lengths[a];
+    std::vector<double2> fwd(static_cast<size_t>(n)), avg(static_cast<size_t>(n));
+    std::vector<double> xi(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) {
+      const size_t sk = size_t(k);
+      if (k == 0) {
+        fwd[sk] = make_double2(0.0, 0.0);
+        avg[sk] = make_double2(1.0, 0.0);
+        xi[sk] = 0.0;
+        continue;
+      }
+      if (2 * k == n) {
+        fwd[sk] = make_double2(-2.0 / h, 0.0);
+        avg[sk] = make_double2(0.0, 0.0);
+        xi[sk] = 2.0 * kPi * double(k) / l;
+        continue;
+      }
+      const double phi = 2.0 * kPi * double(k) / double(n);
+      const double c = std::cos(phi), s = std::sin(phi);
+      fwd[sk] = make_double2((c - 1.0) / h, s / h);
+      avg[sk] = make_double2(0.5 * (c + 1.0), 0.5 * s);
+      const int64_t ks = 2 * k < n ? k : k - n;
+      xi[sk] = 2.0 * kPi * double(ks) / l;
+    }
+    g.fwd[a].alloc(size_t(n));
+    g.avg[a].alloc(size_t(n));
+    g.xi[a].alloc(size_t(n));
+    COMBO_CK(cudaMemcpy(g.fwd[a].p, fwd.data(), size_t(n) * sizeof(double2), cudaMemcpyHostToDevice));
+    COMBO_CK(cudaMemcpy(g.avg[a].p, avg.data(), size_t(n) * sizeof(double2), cudaMemcpyHostToDevice));
+    COMBO_CK(cudaMemcpy(g.xi[a].p, xi.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice));
+  }
+}
+
+GreenTables green_view(const GreenPlan& g) {
+  GreenTables t;
+  t.kind = g.kind;
+  for (int a = 0; a < 3; ++a) {
+    t.fwd[a] = g.fwd[a].p;
+    t.avg[a] = g.avg[a].p;
+    t.xi[a] = g.xi[a].p;
+  }
+  return t;
+}
+}  // namespace
+
+int ew_grid(int64_t n) {
+  const int64_t b = (n + kEwThreads - 1) / kEwThreads;
+  return int(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16)));
+}
+
+void ensure_scratch(combo_ctx* c) {
+  if (!c->dres.p) {
+    c->dres.alloc(64);
+    c->dstats.alloc(1);
+    COMBO_CK(cudaMallocHost(&c->hres, 64 * sizeof(double) + sizeof(Stats)));
+  }
+}
+
+void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
+  for (int a = 0; a < 3; ++a) {
+    if (dims[a] < 1) throw ComboError(COMBO_ERR_BAD_SHAPE, "grid dims must be >= 1");
+    if (!(lengths[a] > 0.0)) throw ComboError(COMBO_ERR_BAD_SHAPE, "grid lengths must be positive");
+  }
+  const std::array<int64_t, 3> d{dims[0], dims[1], dims[2]};
+  const std::array<double, 3> l{lengths[0], lengths[1], lengths[2]};
+  c->has_grid = true;
+  c->dims = d;
+  c->lengths = l;
+  c->N = d[0] * d[1] * d[2];
+  if (c->plan && c->plan->dims == d && c->plan->lengths == l) return;
+  auto p = std::make_unique<FftPlan>();
+  p->dims = d;
+  p->lengths = l;
+  for (int a = 0; a < 3; ++a) build_axis(p->ax[a], int(d[a]));
+  p->n3c = d[2] / 2 + 1;
+  p->n3p = (p->n3c + 7) / 8 * 8;
+  // z pass: L z-lines per block (~1024 cells), pairs of real lines packed
+  const int64_t n3 = d[2];
+  int64_t L = std::max<int64_t>(1, 1024 / n3);
+  while (L > 1 && ((9 * L + 1) / 2) * n3 > 6144) --L;
+  p->zL = int(L);
+  p->zls = int(n3);
+  const int64_t npair = (9 * L + 1) / 2;
+  p->zT = pick_threads(npair * n3);
+  p->zsmem = size_t(npair * n3) * sizeof(double2);
+  // y pass
+  int W = int(std::min<int64_t>(8, p->n3c));
+  while (W > 1 && d[1] * W > 6144) W /= 2;
+  p->yW = W;
+  p->yT = pick_threads(d[1] * W);
+  p->ysmem = size_t(d[1] * W) * sizeof(double2);
+  // x pass + Gamma (3 components per tile)
+  W = int(std::min<int64_t>(8, p->n3c));
+  while (W > 1 && 3 * d[0] * W > 6144) W /= 2;
+  p->xW = W;
+  p->xT = pick_threads(3 * d[0] * W);
+  p->xsmem = size_t(3 * d[0] * W) * sizeof(double2);
+  p->spec.alloc(size_t(9 * d[0] * d[1] * p->n3p));
+  c->plan = std::move(p);
+}
+
+GreenPlan& green_plan(combo_ctx* c, int kind) {
+  if (kind < 0 || kind > 2) throw ComboError(COMBO_ERR_CONFIG_INVALID, "unknown Green operator kind");
+  GreenPlan& g = c->plan->green[kind];
+  if (g.kind != kind) build_green(g, kind, c->plan->dims, c->plan->lengths);
+  return g;
+}
+
+void reduce_partials(combo_ctx* c, int64_t nblocks, int nred, int slot) {
+  ProfScope ps(c, kTagReduce, double(nblocks) * nred * 8.0);
+  k_reduce_partials<<<nred, 1024, 0, c->stream>>>(c->partials.p, nblocks, nred, c->dres.p + slot);
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+}
+
+void fetch_results(combo_ctx* c) {
+  COMBO_CK(cudaMemcpyAsync(c->hres, c->dres.p, 64 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  COMBO_CK(cudaMemcpyAsync(c->hres + 64, c->dstats.p, sizeof(Stats), cudaMemcpyDeviceToHost, c->stream));
+  COMBO_CK(cudaStreamSynchronize(c->stream));
+}
+
+void ensure_partials(combo_ctx* c, int64_t count) {
+  if (c->partials.n < size_t(count)) c->partials.alloc(size_t(count));
+}
+
+// ------------------------------------------------------------- profiler
+namespace {
+cudaEvent_t pool_event(combo_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  COMBO_CK(cudaEventCreate(&e));
+  return e;
+}
+const char* kTagNames[kNumTags] = {"sweep",  "matvec",    "zfwd",      "yfwd",   "xgamma", "yinv",
+                                   "zinv",   "cg_update", "trial",     "materialize", "reduce", "other"};
+}  // namespace
+
+ProfScope::ProfScope(combo_ctx* ctx, int tag, double bytes) : c(ctx) {
+  if (!c->prof_on) return;
+  combo_ctx::ProfRec r{tag, pool_event(c), pool_event(c), bytes};
+  COMBO_CK(cudaEventRecord(r.a, c->stream));
+  idx = int(c->prof.size());
+  c->prof.push_back(r);
+}
+ProfScope::~ProfScope() {
+  if (idx >= 0) cudaEventRecord(c->prof[size_t(idx)].b, c->stream);
+}
+
+double spec_bytes(const combo_ctx* c) {
+  return 9.0 * double(c->plan->dims[0] * c->plan->dims[1] * c->plan->n3c) * 16.0;
+}
+
+// ------------------------------------------------------ launch helpers
+template <class K>
+void smem_attr(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) COMBO_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
+// compile-time line length: log2(n) for powers of two <= 1024, else generic
+template <class F>
+void dispatch_log2(int64_t n, F&& f) {
+  int L = -1;
+  for (int l = 0; l <= 10; ++l)
+    if (n == (int64_t(1) << l)) L = l;
+  switch (L) {
+    case 0: f(std::integral_constant<int, 0>{}); break;
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 5: f(std::integral_constant<int, 5>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    case 7: f(std::integral_constant<int, 7>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    case 9: f(std::integral_constant<int, 9>{}); break;
+    case 10: f(std::integral_constant<int, 10>{}); break;
+    default: f(std::integral_constant<int, kGeneric>{}); break;
+  }
+}
+
+template <class Prod>
+int64_t launch_zfwd(combo_ctx* c, const Prod& prod) {
+  FftPlan& p = *c->plan;
+  const int64_t nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
+  if (Prod::NRED) ensure_partials(c, nb * Prod::NRED);
+  ProfScope ps(c, kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS);
+  dispatch_log2(p.dims[2], [&](auto Lc) {
+    auto k = zfwd_kernel<Prod, decltype(Lc)::value>;
+    smem_attr(k, p.zsmem);
+    k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, prod, c->partials.p);
+  });
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+  return nb;
+}
+
+template <class Cons>
+int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
+  FftPlan& p = *c->plan;
+  const int64_t nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
+  if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
+  const double scale = 1.0 / double(c->N);
+  ProfScope ps(c, kTagZinv, spec_bytes(c) + 72.0 * double(c->N) * Cons::FIELDS);
+  dispatch_log2(p.dims[2], [&](auto Lc) {
+    auto k = zinv_kernel<Cons, decltype(Lc)::value>;
+    smem_attr(k, p.zsmem);
+    k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, scale, cons, c->partials.p);
+  });
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+  return nb;
+}
+
+template <bool INV>
+void launch_y(combo_ctx* c, int ncomp = 9) {
+  FftPlan& p = *c->plan;
+  dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.dims[0]), unsigned(ncomp));
+  ProfScope ps(c, INV ? kTagYinv : kTagYfwd, 2.0 * spec_bytes(c) * ncomp / 9.0);
+  dispatch_log2(p.dims[1], [&](auto Lc) {
+    auto k = ypass_kernel<decltype(Lc)::value, INV>;
+    smem_attr(k, p.ysmem);
+    k<<<grid, p.yT, p.ysmem, c->stream>>>(p.sv(), p.ax[1].view(), p.yW);
+  });
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+}
+
+void launch_xgamma(combo_ctx* c, int kind) {
+  const GreenTables g = green_view(green_plan(c, kind));
+  FftPlan& p = *c->plan;
+  dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 3u);
+  ProfScope ps(c, kTagXGamma, 2.0 * spec_bytes(c));
+  dispatch_log2(p.dims[0], [&](auto Lc) {
+    auto k = xgamma_kernel<decltype(Lc)::value>;
+    smem_attr(k, p.xsmem);
+    k<<<grid, p.xT, p.xsmem, c->stream>>>(p.sv(), p.ax[0].view(), p.xW, g);
+  });
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+}
+
+template <bool INV>
+void launch_x_plain(combo_ctx* c) {
+  FftPlan& p = *c->plan;
+  // plain x pass: x tile geometry with a single component per block
+  const size_t smem = size_t(p.dims[0] * p.xW) * sizeof(double2);
+  dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 9u);
+  dispatch_log2(p.dims[0], [&](auto Lc) {
+    auto k = xpass_kernel<decltype(Lc)::value, INV>;
+    smem_attr(k, smem);
+    k<<<grid, pick_threads(p.dims[0] * p.xW), smem, c->stream>>>(p.sv(), p.ax[0].view(), p.xW);
+  });
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+}
+// Projection Pi(tau) = alpha Gamma^0 tau (green.cpp:133-151) with fused
+// producer / consumer. Returns the partial-block counts via nbp / nbc.
+template <class Prod, class Cons>
+void project_fused(combo_ctx* c, int kind, const Prod& prod, const Cons& cons, int slot_prod, int slot_cons) {
+  const int64_t nbp = launch_zfwd(c, prod);
+  if (Prod::NRED) reduce_partials(c, nbp, Prod::NRED, slot_prod);
+  launch_y<false>(c);
+  launch_xgamma(c, kind);
+  launch_y<true>(c);
+  const int64_t nbc = launch_zinv(c, cons);
+  if (Cons::NRED) reduce_partials(c, nbc, Cons::NRED, slot_cons);
+}
+
+void reset_stats(combo_ctx* c) {
+  COMBO_CK(cudaMemsetAsync(c->dstats.p, 0, sizeof(Stats), c->stream));
+}
+
+// stress sweep: out = P(fin + sh) - alpha (fin + sh); P sums -> slot
+void sweep(combo_ctx* c, const double* fin, const Shift9& sh, double alpha, double* out, bool writeback,
+           int slot) {
+  const int g = ew_grid(c->N);
+  ensure_partials(c, int64_t(g) * 9);
+  {
+    // F read + out write + cid, composite meta (n, c+, c-) and warm r/w
+    ProfScope ps(c, kTagSweep, 148.0 * double(c->N) + 88.0 * double(c->ncomp));
+    k_sweep<<<g, kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, alpha, out, c->N, writeback ? 1 : 0,
+                                             c->dstats.p, c->partials.p);
+  }
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+  reduce_partials(c, g, 9, slot);
+}
+
+Shift9 zero_shift() {
+  Shift9 s;
+  for (double& v : s.v) v = 0.0;
+  return s;
+}
+
+// ------------------------------------------------------- host tensors
+// NH first elasticity tensor at F (closed form A_iJkL, see material.cuh)
+// and Jacobi eigenvalues for the reference-medium choice
+// (materials.cpp:112-125, cell_material.cpp:77-84, solver.cpp:99-104).
+namespace {
+double hdet3(const double* m) {
+  return m[0] * (m[4] * m[8] - m[7] * m[5]) - m[3] * (m[1] * m[8] - m[7] * m[2]) + m[6] * (m[1] * m[5] - m[4] * m[2]);
+}
+bool nh_tangent_host(const combo_law& L, const double* f, double* A) {
+  const double j = hdet3(f);
+  if (!(j > 0.0)) return false;
+  double g[9];
+  g[0] = (f[4] * f[8] - f[5] * f[7]) / j;
+  g[1] = (f[5] * f[6] - f[3] * f[8]) / j;
+  g[2] = (f[3] * f[7] - f[4] * f[6]) / j;
+  g[3] = (f[2] * f[7] - f[1] * f[8]) / j;
+  g[4] = (f[0] * f[8] - f[2] * f[6]) / j;
+  g[5] = (f[1] * f[6] - f[0] * f[7]) / j;
+  g[6] = (f[1] * f[5] - f[2] * f[4]) / j;
+  g[7] = (f[2] * f[3] - f[0] * f[5]) / j;
+  g[8] = (f[0] * f[4] - f[1] * f[3]) / j;
+  const double lnj = std::log(j);
+  const double beta = L.mu - L.lambda * lnj;
+  for (int i = 0; i < 3; ++i)
+    for (int J = 0; J < 3; ++J)
+      for (int k = 0; k < 3; ++k)
+        for (int l = 0; l < 3; ++l)
+          A[9 * (3 * i + J) + 3 * k + l] = (i == k && J == l ? L.mu : 0.0) + L.lambda * g[3 * i + J] * g[3 * k + l] +
+                                           beta * g[3 * i + l] * g[3 * k + J];
+  return true;
+}
+
+void jacobi_eigenvalues(int n, double* a, double* lam) {
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) off += a[p * n + q] * a[p * n + q];
+    if (off == 0.0) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = a[p * n + q];
+        if (apq == 0.0) continue;
+        const double app = a[p * n + p], aqq = a[q * n + q];
+        const double g = 100.0 * std::fabs(apq);
+        if (std::fabs(app) + g == std::fabs(app) && std::fabs(aqq) + g == std::fabs(aqq)) {
+          a[p * n + q] = a[q * n + p] = 0.0;
+          continue;
+        }
+        const double h = aqq - app;
+        double t;
+        if (std::fabs(h) + g == std::fabs(h)) {
+          t = apq / h;
+        } else {
+          const double th = 0.5 * h / apq;
+          t = 1.0 / (std::fabs(th) + std::sqrt(1.0 + th * th));
+          if (th < 0.0) t = -t;
+        }
+        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = t * cs, tau = sn / (1.0 + cs);
+        a[p * n + p] = app - t * apq;
+        a[q * n + q] = aqq + t * apq;
+        a[p * n + q] = a[q * n + p] = 0.0;
+        for (int r = 0; r < n; ++r) {
+          if (r == p || r == q) continue;
+          const double gr = a[r * n + p], hr = a[r * n + q];
+          a[r * n + p] = a[p * n + r] = gr - sn * (hr + gr * tau);
+          a[r * n + q] = a[q * n + r] = hr + sn * (gr - hr * tau);
+        }
+      }
+  }
+  for (int i = 0; i < n; ++i) lam[i] = a[i * n + i];
+  std::sort(lam, lam + n);
+}
+
+void law_bounds(const combo_law& L, const double* f, double& lo, double& hi) {
+  if (L.kind == COMBO_LAW_LINEAR) {
+    double a[36], lam[6];
+    std::memcpy(a, L.c6, sizeof a);
+    jacobi_eigenvalues(6, a, lam);
+    lo = std::min(0.0, lam[0]);
+    hi = lam[5];
+    return;
+  }
+  double A[81];
+  if (!nh_tangent_host(L, f, A)) {
+    lo = L.mu;
+    hi = L.lambda + 2.0 * L.mu;
+    return;
+  }
+  double s[81], lam[9];
+  for (int i = 0; i < 9; ++i)
+    for (int j = 0; j < 9; ++j) s[9 * i + j] = 0.5 * (A[9 * i + j] + A[9 * j + i]);
+  jacobi_eigenvalues(9, s, lam);
+  lo = lam[0];
+  hi = lam[8];
+}
+}  // namespace
+
+void spectrum_bounds(const combo_ctx* c, const double* fbar, double& lo, double& hi) {
+  double l0, h0, l1, h1;
+  law_bounds(c->law_m, fbar, l0, h0);
+  law_bounds(c->law_i, fbar, l1, h1);
+  lo = std::min(l0, l1);
+  hi = std::max(h0, h1);
+}
+
+// mandel_to_mat9 (tensor.cpp:127-136) for the linear law
+void mandel_to_mat9(const double* c6, double* a9) {
+  static const int pair[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {0, 2}, {1, 2}};
+  const double s2 = 1.4142135623730951;
+  double full[81] = {0};
+  for (int a = 0; a < 6; ++a)
+    for (int b = 0; b < 6; ++b) {
+      const int i = pair[a][0], j = pair[a][1], k = pair[b][0], l = pair[b][1];
+      const double v = c6[6 * a + b] / ((a < 3 ? 1.0 : s2) * (b < 3 ? 1.0 : s2));
+      full[((i * 3 + j) * 3 + k) * 3 + l] = v;
+      full[((j * 3 + i) * 3 + k) * 3 + l] = v;
+      full[((i * 3 + j) * 3 + l) * 3 + k] = v;
+      full[((j * 3 + i) * 3 + l) * 3 + k] = v;
+    }
+  for (int i = 0; i < 81; ++i) a9[i] = full[i];
+}
+
+// dev_a9: 81 doubles of device memory owned by the caller (linear law only)
+LawP law_params(const combo_law& L, double* dev_a9) {
+  LawP p{};
+  p.kind = L.kind;
+  p.lambda = L.lambda;
+  p.mu = L.mu;
+  p.a9 = nullptr;
+  if (L.kind == COMBO_LAW_LINEAR) {
+    double a9[81];
+    mandel_to_mat9(L.c6, a9);
+    COMBO_CK(cudaMemcpy(dev_a9, a9, sizeof a9, cudaMemcpyHostToDevice));
+    p.a9 = dev_a9;
+  }
+  return p;
+}
+
+// ------------------------------------------------------------------ solver
+namespace {
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t) { return std::chrono::duration<double>(Clock::now() - t).count(); }
+double norm9(const double* m) {
+  double s = 0.0;
+  for (int i = 0; i < 9; ++i) s += m[i] * m[i];
+  return std::sqrt(s);
+}
+struct LsBudget {};
+}  // namespace
+
+// Field slots of the solver (9N doubles each), cached on the context.
+struct SolverFields {
+  DBuf<double> f[9];
+};
+
+class Solver {
+ public:
+  Solver(combo_ctx* c, const combo_solver_cfg& cfg) : c_(c), cfg_(cfg), N_(c->N) {
+    ensure_scratch(c);
+    for (int i = 0; i < 8; ++i) bufs_[i].alloc(size_t(9 * N_));
+    F_ = bufs_[0].p;
+    Fo_ = bufs_[1].p;  // basic: F_new ; newton: F_trial
+    x_ = bufs_[2].p;
+    r_ = bufs_[3].p;
+    pd_ = bufs_[4].p;
+    ap_ = bufs_[5].p;
+    rb_ = bufs_[6].p;
+    bn_ = bufs_[7].p;
+    double lo, hi;
+    const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    spectrum_bounds(c, I, lo, hi);
+    stress_floor_ = 1e-12 * std::max(hi, 1e-12);
+    shF_ = zero_shift();
+  }
+
+  void run(const double* fbar_target, combo_report& rep);
+  double* F() { return F_; }
+  Shift9 shiftF() const { return shF_; }
+  const double* pbar() const { return pbar_; }
+  void final_stress(double* P);
+  void materialize();
+
+ private:
+  bool run_step(const double* fbar, combo_host::StepRec& rep);
+  bool run_basic(const double* fbar, combo_host::StepRec& rep);
+  bool run_newton(const double* fbar, combo_host::StepRec& rep);
+  int cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::StepRec& rep);
+  void count_ls() {
+    if (cfg_.max_ls_iterations > 0 && ls_total_ >= cfg_.max_ls_iterations) throw LsBudget{};
+    ++ls_total_;
+  }
+  combo_sweep_stats stats() const {
+    const Stats* s = reinterpret_cast<const Stats*>(c_->hres + 64);
+    combo_sweep_stats o;
+    o.inadmissible_cells = int64_t(s->inadmissible);
+    o.laminate_failures = int64_t(s->failures);
+    o.back_projections = int64_t(s->backproj);
+    o.laminate_iter_max = int64_t(s->iter_max);
+    return o;
+  }
+  // pin_mean on F (field.cpp:28-38): materialize pending shift, sum, new shift
+  void pin_mean(const double* target) {
+    const int g = ew_grid(N_);
+    ensure_partials(c_, int64_t(g) * 9);
+    {
+      ProfScope ps(c_, kTagMaterialize, 144.0 * double(N_));
+      k_materialize<<<g, kEwThreads, 0, c_->stream>>>(F_, shF_, N_, c_->partials.p);
+    }
+    ++c_->launches;
+    COMBO_CK(cudaGetLastError());
+    reduce_partials(c_, g, 9, 0);
+    fetch_results(c_);
+    for (int q = 0; q < 9; ++q) shF_.v[q] = target[q] - c_->hres[q] / double(N_);
+  }
+
+ public:
+  combo_ctx* c_;
+  combo_solver_cfg cfg_;
+  int64_t N_;
+  DBuf<double> bufs_[8];
+  double *F_, *Fo_, *x_, *r_, *pd_, *ap_, *rb_, *bn_;
+  Shift9 shF_;
+  double alpha_ = 1.0;
+  double stress_floor_;
+  double pbar_[9] = {0};
+  int64_t ls_total_ = 0;
+  const double* last_eval_ = nullptr;
+  Shift9 last_eval_shift_;
+};
+
+void Solver::materialize() {
+  const int g = ew_grid(N_);
+  ensure_partials(c_, int64_t(g) * 9);
+  k_materialize<<<g, kEwThreads, 0, c_->stream>>>(F_, shF_, N_, c_->partials.p);
+  ++c_->launches;
+  COMBO_CK(cudaGetLastError());
+  shF_ = zero_shift();
+}
+
+// run_basic (solver.cpp:124-164)
+bool Solver::run_basic(const double* fbar, combo_host::StepRec& rep) {
+  double lo, hi;
+  spectrum_bounds(c_, fbar, lo, hi);  // pick_alpha (:99-104)
+  alpha_ = 0.5 * (std::max(lo, 0.0) + hi);
+  if (!(alpha_ > 0.0)) alpha_ = std::max(hi, 1.0);
+  for (int it = 1; it <= cfg_.max_outer; ++it) {
+    reset_stats(c_);
+    sweep(c_, F_, shF_, alpha_, rb_, true, 0);  // tau = P - alpha F ; P sums -> slot 0
+    last_eval_ = F_;
+    last_eval_shift_ = shF_;
+    ConsBasic cons;
+    cons.fold = F_;
+    cons.fold_shift = shF_;
+    cons.fnew = Fo_;
+    for (int q = 0; q < 9; ++q) cons.fbar.v[q] = fbar[q];
+    cons.alpha = alpha_;
+    cons.N = N_;
+    ProdLoad9 prod{rb_, N_};
+    project_fused(c_, cfg_.green, prod, cons, 0, 9);  // diff^2 -> 9, F_new sums -> 10..18
+    fetch_results(c_);
+    rep.sweep = stats();
+    if (rep.sweep.inadmissible_cells > 0) return false;
+    count_ls();
+    ++rep.ls_basic;
+    for (int q = 0; q < 9; ++q) pbar_[q] = c_->hres[q] / double(N_);
+    rep.pbar_history.push_back({});
+    std::memcpy(rep.pbar_history.back().data(), pbar_, sizeof pbar_);
+    const double resid = alpha_ * std::sqrt(c_->hres[9] / double(N_)) / std::max(norm9(pbar_), stress_floor_);
+    rep.residuals.push_back(resid);
+    rep.cg_iters.push_back(0);
+    rep.outer_iters = it;
+    if (cfg_.verbose) std::printf("  basic it %3d resid %.3e\n", it, resid);
+    std::swap(F_, Fo_);
+    for (int q = 0; q < 9; ++q) shF_.v[q] = fbar[q] - c_->hres[10 + q] / double(N_);
+    if (rep.sweep.laminate_failures > 0 && resid <= cfg_.tol_equilibrium) return false;
+    if (resid <= cfg_.tol_equilibrium) {
+      rep.converged = true;
+      return true;
+    }
+  }
+  return false;
+}
+
+// cg_solve (solver.cpp:166-200); r holds b on entry, x is zeroed here
+int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::StepRec& rep) {
+  breakdown = false;
+  COMBO_CK(cudaMemsetAsync(x_, 0, size_t(9 * N_) * sizeof(double), c_->stream));
+  double rr = rr0;
+  const double bnorm = std::sqrt(rr);
+  if (bnorm == 0.0) return 0;
+  int it = 0;
+  double beta = 0.0;
+  const int g = ew_grid(N_);
+  while (it < cfg_.cg_max) {
+    {
+      // r, pdir (r/w), F, q and cid; composite n, c+-, a
+      ProfScope ps(c_, kTagMatvec, (it == 0 ? 292.0 : 364.0) * double(N_) + 64.0 * double(c_->ncomp));
+      k_matvec<<<g, kEwThreads, 0, c_->stream>>>(c_->mp, c_->cell_data(), F_, shF_, r_, pd_, beta,
+                                                  it == 0 ? 1 : 0, rb_, N_);
+    }
+    ++c_->launches;
+    COMBO_CK(cudaGetLastError());
+    ProdLoad9 prod{rb_, N_};
+    ConsCg cons{ap_, pd_, N_};
+    count_ls();
+    ++rep.ls_cg;
+    project_fused(c_, cfg_.green, prod, cons, 0, 20);
+    fetch_results(c_);
+    const double pap = c_->hres[20];
+    if (!(pap > 0.0)) {
+      breakdown = true;
+      return it;
+    }
+    const double step = rr / pap;
+    ensure_partials(c_, g);
+    {
+      ProfScope ps(c_, kTagCgUpdate, 432.0 * double(N_));
+      k_cg_update<<<g, kEwThreads, 0, c_->stream>>>(x_, r_, pd_, ap_, step, 9 * N_, c_->partials.p);
+    }
+    ++c_->launches;
+    COMBO_CK(cudaGetLastError());
+    reduce_partials(c_, g, 1, 21);
+    fetch_results(c_);
+    ++it;
+    const double rr_new = c_->hres[21];
+    if (std::sqrt(rr_new) <= tol_rel * bnorm) return it;
+    beta = rr_new / rr;
+    rr = rr_new;
+  }
+  return it;
+}
+
+// run_newton (solver.cpp:202-259) with the accepted trial's residual reused
+// as the next Newton residual (bitwise identical when the trial sweep had no
+// laminate failures; still counted as an LS iteration).
+bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
+  bool reuse = false;
+  double reuse_ss = 0.0, reuse_pbar[9];
+  for (int it = 1; it <= cfg_.max_outer; ++it) {
+    double ss;
+    if (!reuse) {
+      reset_stats(c_);
+      sweep(c_, F_, shF_, 0.0, rb_, true, 0);
+      last_eval_ = F_;
+      last_eval_shift_ = shF_;
+      fetch_results(c_);
+      rep.sweep = stats();
+      if (rep.sweep.inadmissible_cells > 0) return false;
+      for (int q = 0; q < 9; ++q) pbar_[q] = c_->hres[q] / double(N_);
+      count_ls();
+      ++rep.ls_residual;
+      ProdLoad9 prod{rb_, N_};
+      ConsResid cons{r_, N_};
+      project_fused(c_, cfg_.green, prod, cons, 0, 9);
+      fetch_results(c_);
+      ss = c_->hres[9];
+    } else {
+      rep.sweep = combo_sweep_stats{0, 0, 0, 0};
+      std::memcpy(pbar_, reuse_pbar, sizeof pbar_);
+      count_ls();
+      ++rep.ls_residual;
+      std::swap(r_, bn_);
+      ss = reuse_ss;
+    }
+    rep.pbar_history.push_back({});
+    std::memcpy(rep.pbar_history.back().data(), pbar_, sizeof pbar_);
+    const double den = std::max(norm9(pbar_), stress_floor_);
+    const double resid = std::sqrt(ss / double(N_)) / den;
+    rep.residuals.push_back(resid);
+    rep.outer_iters = it;
+    if (cfg_.verbose) std::printf("  newton it %3d resid %.3e\n", it, resid);
+    if (resid <= cfg_.tol_equilibrium) {
+      rep.cg_iters.push_back(0);
+      rep.converged = rep.sweep.laminate_failures == 0;
+      return rep.converged;
+    }
+    const double eta = std::max(std::min(cfg_.cg_tol, std::sqrt(resid)), 1e-8);
+    bool breakdown = false;
+    const int cg_its = cg_solve(eta, ss, breakdown, rep);
+    rep.cg_iters.push_back(cg_its);
+    if (breakdown) {
+      ++rep.cg_breakdowns;
+      if (cg_its == 0) return false;
+    }
+    // backtracking line search (:238-255)
+    double s = 1.0;
+    bool accepted = false;
+    combo_sweep_stats st_acc{};
+    double ss_acc = 0.0;
+    Shift9 sh_t{};
+    for (int ls = 0; ls < 10; ++ls) {
+      const int g = ew_grid(N_);
+      ensure_partials(c_, int64_t(g) * 9);
+      {
+        ProfScope ps(c_, kTagTrial, 216.0 * double(N_));
+        k_trial<<<g, kEwThreads, 0, c_->stream>>>(F_, shF_, x_, s, Fo_, N_, c_->partials.p);
+      }
+      ++c_->launches;
+      COMBO_CK(cudaGetLastError());
+      reduce_partials(c_, g, 9, 30);
+      fetch_results(c_);
+      for (int q = 0; q < 9; ++q) sh_t.v[q] = fbar[q] - c_->hres[30 + q] / double(N_);
+      reset_stats(c_);
+      sweep(c_, Fo_, sh_t, 0.0, rb_, true, 0);
+      last_eval_ = Fo_;
+      last_eval_shift_ = sh_t;
+      fetch_results(c_);
+      const combo_sweep_stats st = stats();
+      if (st.inadmissible_cells == 0) {
+        double pb[9];
+        for (int q = 0; q < 9; ++q) pb[q] = c_->hres[q] / double(N_);
+        count_ls();
+        ++rep.ls_trial;
+        ProdLoad9 prod{rb_, N_};
+        ConsResid cons{bn_, N_};
+        project_fused(c_, cfg_.green, prod, cons, 0, 9);
+        fetch_results(c_);
+        const double ss_t = c_->hres[9];
+        std::memcpy(pbar_, pb, sizeof pb);  // residual_from_stress sets pbar_ (:95)
+        const double rtrial = std::sqrt(ss_t / double(N_)) / std::max(norm9(pb), stress_floor_);
+        if (rtrial <= resid * (1.0 + 1e-12)) {
+          accepted = true;
+          st_acc = st;
+          ss_acc = ss_t;
+          std::memcpy(reuse_pbar, pb, sizeof pb);
+          break;
+        }
+      }
+      s *= 0.5;
+      ++rep.line_search_cuts;
+    }
+    if (!accepted) return false;
+    std::swap(F_, Fo_);
+    shF_ = sh_t;
+    if (last_eval_ == Fo_) last_eval_ = F_;
+    reuse = st_acc.laminate_failures == 0;
+    reuse_ss = ss_acc;
+  }
+  return false;
+}
+
+bool Solver::run_step(const double* fbar, combo_host::StepRec& rep) {
+  return cfg_.scheme == COMBO_SCHEME_BASIC ? run_basic(fbar, rep) : run_newton(fbar, rep);
+}
+
+// solve (solver.cpp:286-346)
+void Solver::run(const double* fbar_target, combo_report& report) {
+  const auto tic = Clock::now();
+  const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  double h[9];
+  for (int q = 0; q < 9; ++q) h[q] = fbar_target[q] - I[q];
+  double t = 0.0;
+  double dt = 1.0 / cfg_.load_steps;
+  double fbar_prev[9];
+  std::memcpy(fbar_prev, I, sizeof I);
+  {
+    Shift9 one;
+    for (int q = 0; q < 9; ++q) one.v[q] = I[q];
+    k_fill9<<<ew_grid(N_), kEwThreads, 0, c_->stream>>>(F_, one, N_);
+    ++c_->launches;
+  }
+  shF_ = zero_shift();
+  report.success = true;
+  DBuf<double> backup_f, backup_warm;
+  backup_f.alloc(size_t(9 * N_));
+  if (c_->ncomp) backup_warm.alloc(size_t(3 * c_->ncomp));
+  try {
+    while (t < 1.0 - 1e-12) {
+      const double dt_try = std::min(dt, 1.0 - t);
+      double fbar[9];
+      for (int q = 0; q < 9; ++q) fbar[q] = I[q] + (t + dt_try) * h[q];
+      // backup F (materialized) and warm starts
+      materialize();
+      COMBO_CK(cudaMemcpyAsync(backup_f.p, F_, size_t(9 * N_) * sizeof(double), cudaMemcpyDeviceToDevice, c_->stream));
+      if (c_->ncomp)
+        COMBO_CK(cudaMemcpyAsync(backup_warm.p, c_->warm.p, size_t(3 * c_->ncomp) * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c_->stream));
+      pin_mean(fbar);
+      combo_host::StepRec rep;
+      rep.t_start = t;
+      rep.t_end = t + dt_try;
+      std::memcpy(rep.fbar, fbar, sizeof fbar);
+      const auto st0 = Clock::now();
+      const bool ok = run_step(fbar, rep);
+      rep.converged = ok;
+      rep.seconds = since(st0);
+      if (ok) {
+        report.steps.push_back(std::move(rep));
+        t += dt_try;
+        std::memcpy(fbar_prev, fbar, sizeof fbar);
+        continue;
+      }
+      COMBO_CK(cudaMemcpyAsync(F_, backup_f.p, size_t(9 * N_) * sizeof(double), cudaMemcpyDeviceToDevice, c_->stream));
+      shF_ = zero_shift();
+      pin_mean(fbar_prev);
+      if (c_->ncomp)
+        COMBO_CK(cudaMemcpyAsync(c_->warm.p, backup_warm.p, size_t(3 * c_->ncomp) * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c_->stream));
+      ++report.bisections;
+      if (report.bisections > cfg_.max_bisections) {
+        report.steps.push_back(std::move(rep));
+        report.success = false;
+        report.error = "LoadPathFailed: bisection budget exhausted";
+        break;
+      }
+      dt = 0.5 * dt_try;
+    }
+  } catch (const LsBudget&) {
+    report.success = false;
+    report.error = "LsBudgetExhausted";
+  }
+  COMBO_CK(cudaStreamSynchronize(c_->stream));
+  report.alpha = alpha_;
+  report.ls_total = ls_total_;
+  report.seconds_total = since(tic);
+}
+
+void Solver::final_stress(double* P) {
+  const double* fin = last_eval_ ? last_eval_ : F_;
+  const Shift9 sh = last_eval_ ? last_eval_shift_ : shF_;
+  reset_stats(c_);
+  sweep(c_, fin, sh, 0.0, P, false, 40);
+}
+
+std::string report_json(const combo_report& r) {
+  auto fmt = [](double v) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    return std::string(b);
+  };
+  std::ostringstream js;
+  js << "{\"success\":" << (r.success ? "true" : "false") << ",\"error\":\"" << r.error
+     << "\",\"bisections\":" << r.bisections << ",\"alpha\":" << fmt(r.alpha)
+     << ",\"seconds_total\":" << fmt(r.seconds_total) << ",\"ls_total\":" << r.ls_total << ",\"steps\":[";
+  for (size_t s = 0; s < r.steps.size(); ++s) {
+    const auto& st = r.steps[s];
+    if (s) js << ",";
+    js << "{\"t_start\":" << fmt(st.t_start) << ",\"t_end\":" << fmt(st.t_end)
+       << ",\"converged\":" << (st.converged ? "true" : "false") << ",\"outer_iters\":" << st.outer_iters
+       << ",\"cg_breakdowns\":" << st.cg_breakdowns << ",\"line_search_cuts\":" << st.line_search_cuts
+       << ",\"seconds\":" << fmt(st.seconds) << ",\"ls_basic\":" << st.ls_basic << ",\"ls_residual\":" << st.ls_residual
+       << ",\"ls_cg\":" << st.ls_cg << ",\"ls_trial\":" << st.ls_trial << ",\"fbar\":[";
+    for (int i = 0; i < 9; ++i) js << (i ? "," : "") << fmt(st.fbar[i]);
+    js << "],\"residuals\":[";
+    for (size_t i = 0; i < st.residuals.size(); ++i) js << (i ? "," : "") << fmt(st.residuals[i]);
+    js << "],\"cg_iters\":[";
+    for (size_t i = 0; i < st.cg_iters.size(); ++i) js << (i ? "," : "") << st.cg_iters[i];
+    js << "],\"pbar_history\":[";
+    for (size_t i = 0; i < st.pbar_history.size(); ++i) {
+      js << (i ? "," : "") << "[";
+      for (int q = 0; q < 9; ++q) js << (q ? "," : "") << fmt(st.pbar_history[i][size_t(q)]);
+      js << "]";
+    }
+    js << "],\"sweep\":{\"inadmissible\":" << st.sweep.inadmissible_cells << ",\"failures\":" << st.sweep.laminate_failures
+       << ",\"back_projections\":" << st.sweep.back_projections << ",\"iter_max\":" << st.sweep.laminate_iter_max << "}}";
+  }
+  js << "]}";
+  return js.str();
+}
+
+}  // namespace combo_host
+
+// ====================================================================== C-ABI
+using namespace combo_host;
+
+namespace {
+template <class Fn>
+int guarded(combo_ctx* c, Fn&& fn) {
+  try {
+    if (c) COMBO_CK(cudaSetDevice(c->device));
+    fn();
+    return COMBO_OK;
+  } catch (const ComboError& e) {
+    if (c) c->err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (c) c->err = "host allocation failed";
+    return COMBO_ERR_OOM;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return COMBO_ERR_BAD_ARGUMENT;
+  }
+}
+
+void require_bound(const combo_ctx* c) {
+  if (!c->bound) throw ComboError(COMBO_ERR_STATE, "materials not bound (combo_bind_materials)");
+}
+
+// stage a 9N field to the device (returns device pointer)
+const double* stage_in(combo_ctx* c, const double* p, int mem, int slot) {
+  if (mem == COMBO_MEM_DEVICE) return p;
+  c->scratch[slot].alloc(size_t(9 * c->N));
+  COMBO_CK(cudaMemcpyAsync(c->scratch[slot].p, p, size_t(9 * c->N) * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  return c->scratch[slot].p;
+}
+double* stage_out(combo_ctx* c, double* p, int mem, int slot) {
+  if (mem == COMBO_MEM_DEVICE) return p;
+  c->scratch[slot].alloc(size_t(9 * c->N));
+  return c->scratch[slot].p;
+}
+void finish_out(combo_ctx* c, double* host, const double* dev, int mem, size_t count) {
+  if (mem == COMBO_MEM_DEVICE) return;
+  COMBO_CK(cudaMemcpyAsync(host, dev, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  COMBO_CK(cudaStreamSynchronize(c->stream));
+}
+}  // namespace
+
+extern "C" {
+
+const char* combo_version(void) { return "combo-b200 0.1 (sm_100a, fp64)"; }
+
+int combo_ctx_create(int device, combo_ctx** out) {
+  if (!out) return COMBO_ERR_BAD_ARGUMENT;
+  *out = nullptr;
+  auto* c = new combo_ctx();
+  c->device = device;
+  const int rc = guarded(c, [&] {
+    int n = 0;
+    COMBO_CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "no such CUDA device");
+    COMBO_CK(cudaSetDevice(device));
+    COMBO_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    ensure_scratch(c);
+  });
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return COMBO_OK;
+}
+
+int combo_ctx_destroy(combo_ctx* c) {
+  if (!c) return COMBO_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  c->plan.reset();
+  if (c->hres) cudaFreeHost(c->hres);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return COMBO_OK;
+}
+
+const char* combo_last_error(const combo_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int combo_kernel_launches(const combo_ctx* c, int64_t* count) {
+  if (!c || !count) return COMBO_ERR_BAD_ARGUMENT;
+  *count = c->launches;
+  return COMBO_OK;
+}
+
+int combo_synchronize(combo_ctx* c) {
+  return guarded(c, [&] { COMBO_CK(cudaStreamSynchronize(c->stream)); });
+}
+
+int combo_profile_enable(combo_ctx* c, int enable) {
+  return guarded(c, [&] {
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+    for (auto& r : c->prof) {
+      c->ev_pool.push_back(r.a);
+      c->ev_pool.push_back(r.b);
+    }
+    c->prof.clear();
+    c->prof_on = enable != 0;
+  });
+}
+
+const char* combo_profile_json(combo_ctx* c) {
+  const int rc = guarded(c, [&] {
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+    double ms[kNumTags] = {0}, bytes[kNumTags] = {0};
+    int64_t n[kNumTags] = {0};
+    for (const auto& r : c->prof) {
+      float t = 0.f;
+      COMBO_CK(cudaEventElapsedTime(&t, r.a, r.b));
+      ms[r.tag] += double(t);
+      bytes[r.tag] += r.bytes;
+      ++n[r.tag];
+    }
+    std::ostringstream js;
+    js << "{";
+    bool first = true;
+    for (int t = 0; t < kNumTags; ++t) {
+      if (!n[t]) continue;
+      char b[256];
+      std::snprintf(b, sizeof b, "%s\"%s\":{\"launches\":%lld,\"ms\":%.6f,\"bytes\":%.6e}", first ? "" : ",",
+                    kTagNames[t], (long long)n[t], ms[t], bytes[t]);
+      js << b;
+      first = false;
+    }
+    js << "}";
+    c->prof_json = js.str();
+  });
+  if (rc) c->prof_json = "{}";
+  return c->prof_json.c_str();
+}
+
+int combo_set_grid(combo_ctx* c, const int64_t dims[3], const double lengths[3]) {
+  return guarded(c, [&] { set_grid(c, dims, lengths); });
+}
+
+// CellMaterials::CellMaterials (cell_material.cpp:12-55)
+int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengths[3], const uint8_t* kind,
+                         const double* c_plus, const double* normal3, const combo_law* matrix,
+                         const combo_law* inclusion, int combo, const combo_laminate_opts* lam, int mem) {
+  return guarded(c, [&] {
+    if (!kind || !c_plus || !matrix || !inclusion) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
+    set_grid(c, dims, lengths);
+    const int64_t N = c->N;
+    std::vector<uint8_t> hk(static_cast<size_t>(N));
+    std::vector<double> hc(static_cast<size_t>(N)), hn;
+    if (mem == COMBO_MEM_DEVICE) {
+      COMBO_CK(cudaMemcpy(hk.data(), kind, size_t(N), cudaMemcpyDeviceToHost));
+      COMBO_CK(cudaMemcpy(hc.data(), c_plus, size_t(N) * 8, cudaMemcpyDeviceToHost));
+    } else {
+      std::memcpy(hk.data(), kind, size_t(N));
+      std::memcpy(hc.data(), c_plus, size_t(N) * 8);
+    }
+    const double* nptr = normal3;
+    if (normal3 && mem == COMBO_MEM_DEVICE) {
+      hn.resize(size_t(3 * N));
+      COMBO_CK(cudaMemcpy(hn.data(), normal3, size_t(3 * N) * 8, cudaMemcpyDeviceToHost));
+      nptr = hn.data();
+    }
+    combo_laminate_opts opts{0.0, 1e-10, 0.0, 50, 1, 0.0};
+    if (lam) opts = *lam;
+    std::vector<int32_t> cid(static_cast<size_t>(N));
+    std::vector<double> nx, ny, nz, cp, cm;
+    for (int64_t i = 0; i < N; ++i) {
+      const size_t si = size_t(i);
+      if (hk[si] == 0) {
+        cid[si] = -1;
+      } else if (hk[si] == 1) {
+        cid[si] = -2;
+      } else {
+        const double cpl = hc[si];
+        if (combo && cpl >= opts.c_min && 1.0 - cpl >= opts.c_min) {
+          // ComboMeta::make (laminate.cpp:28-34)
+          if (!(cpl > 0.0) || !(cpl < 1.0))
+            throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ComboMeta: volume fraction must lie in (0,1)");
+          if (!nptr) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ComboMeta: zero normal");
+          const double a = nptr[3 * si], b = nptr[3 * si + 1], d = nptr[3 * si + 2];
+          const double len = std::sqrt(a * a + b * b + d * d);
+          if (!(len > 0.0)) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ComboMeta: zero normal");
+          cid[si] = int32_t(nx.size());
+          nx.push_back(a / len);
+          ny.push_back(b / len);
+          nz.push_back(d / len);
+          cp.push_back(cpl);
+          cm.push_back(1.0 - cpl);
+        } else {
+          cid[si] = cpl >= 0.5 ? -2 : -1;
+        }
+      }
+    }
+    c->ncomp = int64_t(nx.size());
+    c->cid.alloc(size_t(N));
+    COMBO_CK(cudaMemcpy(c->cid.p, cid.data(), size_t(N) * 4, cudaMemcpyHostToDevice));
+    const size_t nc = size_t(std::max<int64_t>(c->ncomp, 1));
+    c->nrm.alloc(3 * nc);
+    c->cp.alloc(nc);
+    c->cm.alloc(nc);
+    c->warm.alloc(3 * nc);
+    if (c->ncomp) {
+      COMBO_CK(cudaMemcpy(c->nrm.p, nx.data(), nx.size() * 8, cudaMemcpyHostToDevice));
+      COMBO_CK(cudaMemcpy(c->nrm.p + c->ncomp, ny.data(), ny.size() * 8, cudaMemcpyHostToDevice));
+      COMBO_CK(cudaMemcpy(c->nrm.p + 2 * c->ncomp, nz.data(), nz.size() * 8, cudaMemcpyHostToDevice));
+      COMBO_CK(cudaMemcpy(c->cp.p, cp.data(), cp.size() * 8, cudaMemcpyHostToDevice));
+      COMBO_CK(cudaMemcpy(c->cm.p, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice));
+    }
+    COMBO_CK(cudaMemset(c->warm.p, 0, 3 * nc * 8));
+    c->law_m = *matrix;
+    c->law_i = *inclusion;
+    c->lam = opts;
+    double lo, hi;
+    const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    spectrum_bounds(c, I, lo, hi);
+    c->stress_floor = 1e-12 * std::max(hi, 1e-12);
+    if (c->lam.stress_floor == 0.0) c->lam.stress_floor = c->stress_floor;
+    c->a9.alloc(162);
+    c->mp.law[0] = law_params(c->law_m, c->a9.p);
+    c->mp.law[1] = law_params(c->law_i, c->a9.p + 81);
+    c->mp.lam.tol_abs = c->lam.tol_abs;
+    c->mp.lam.tol_rel = c->lam.tol_rel;
+    c->mp.lam.stress_floor = c->lam.stress_floor;
+    c->mp.lam.max_iter = c->lam.max_iter;
+    c->mp.lam.back_projection = c->lam.back_projection;
+    c->dfmg_warm.release();
+    c->bound = true;
+  });
+}
+
+int combo_composite_cells(const combo_ctx* c, int64_t* count) {
+  if (!c || !count) return COMBO_ERR_BAD_ARGUMENT;
+  *count = c->ncomp;
+  return COMBO_OK;
+}
+
+int combo_stress_floor(const combo_ctx* c, double* f) {
+  if (!c || !f) return COMBO_ERR_BAD_ARGUMENT;
+  *f = c->lam.stress_floor;
+  return COMBO_OK;
+}
+
+int combo_spectrum_bounds(combo_ctx* c, const double fbar[9], double* lo, double* hi) {
+  return guarded(c, [&] {
+    require_bound(c);
+    spectrum_bounds(c, fbar, *lo, *hi);
+  });
+}
+
+int combo_get_warm_starts(combo_ctx* c, double* warm3, int mem) {
+  return guarded(c, [&] {
+    require_bound(c);
+    const int64_t n = c->ncomp;
+    if (!n) return;
+    std::vector<double> soa(size_t(3 * n));
+    COMBO_CK(cudaMemcpy(soa.data(), c->warm.p, soa.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<double> aos(size_t(3 * n));
+    for (int64_t i = 0; i < n; ++i)
+      for (int d = 0; d < 3; ++d) aos[size_t(3 * i + d)] = soa[size_t(d * n + i)];
+    if (mem == COMBO_MEM_DEVICE)
+      COMBO_CK(cudaMemcpy(warm3, aos.data(), aos.size() * 8, cudaMemcpyHostToDevice));
+    else
+      std::memcpy(warm3, aos.data(), aos.size() * 8);
+  });
+}
+
+int combo_set_warm_starts(combo_ctx* c, const double* warm3, int mem) {
+  return guarded(c, [&] {
+    require_bound(c);
+    const int64_t n = c->ncomp;
+    if (!n) return;
+    std::vector<double> aos(size_t(3 * n));
+    if (mem == COMBO_MEM_DEVICE)
+      COMBO_CK(cudaMemcpy(aos.data(), warm3, aos.size() * 8, cudaMemcpyDeviceToHost));
+    else
+      std::memcpy(aos.data(), warm3, aos.size() * 8);
+    std::vector<double> soa(size_t(3 * n));
+    for (int64_t i = 0; i < n; ++i)
+      for (int d = 0; d < 3; ++d) soa[size_t(d * n + i)] = aos[size_t(3 * i + d)];
+    COMBO_CK(cudaMemcpy(c->warm.p, soa.data(), soa.size() * 8, cudaMemcpyHostToDevice));
+  });
+}
+
+int combo_stress_sweep(combo_ctx* c, const double* F, double* P, combo_sweep_stats* st, int mem) {
+  return guarded(c, [&] {
+    require_bound(c);
+    ensure_scratch(c);
+    const double* f = stage_in(c, F, mem, 0);
+    double* p = stage_out(c, P, mem, 1);
+    reset_stats(c);
+    sweep(c, f, zero_shift(), 0.0, p, true, 0);
+    fetch_results(c);
+    finish_out(c, P, p, mem, size_t(9 * c->N));
+    if (st) {
+      const Stats* s = reinterpret_cast<const Stats*>(c->hres + 64);
+      st->inadmissible_cells = int64_t(s->inadmissible);
+      st->laminate_failures = int64_t(s->failures);
+      st->back_projections = int64_t(s->backproj);
+      st->laminate_iter_max = int64_t(s->iter_max);
+    }
+  });
+}
+
+int combo_tangent_matvec(combo_ctx* c, const double* F, const double* x, double* y, int mem) {
+  return guarded(c, [&] {
+    require_bound(c);
+    const double* f = stage_in(c, F, mem, 0);
+    const double* xx = stage_in(c, x, mem, 1);
+    double* yy = stage_out(c, y, mem, 2);
+    c->scratch[3].alloc(size_t(9 * c->N));
+    k_matvec<<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), f, zero_shift(), xx,
+                                                           c->scratch[3].p, 0.0, 1, yy, c->N);
+    ++c->launches;
+    COMBO_CK(cudaGetLastError());
+    finish_out(c, y, yy, mem, size_t(9 * c->N));
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int combo_tangent45(combo_ctx* c, const double* F, double* t45, int mem) {
+  return guarded(c, [&] {
+    require_bound(c);
+    const double* f = stage_in(c, F, mem, 0);
+    DBuf<double> t;
+    double* dt = t45;
+    if (mem != COMBO_MEM_DEVICE) {
+      t.alloc(size_t(45 * c->N));
+      dt = t.p;
+    }
+    k_tangent45<<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), f, dt, c->N);
+    ++c->launches;
+    COMBO_CK(cudaGetLastError());
+    finish_out(c, t45, dt, mem, size_t(45 * c->N));
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int combo_tangent45_matvec(combo_ctx* c, const double* t45, const double* x, double* y, int mem) {
+  return guarded(c, [&] {
+    if (!c->has_grid) throw ComboError(COMBO_ERR_STATE, "no grid");
+    DBuf<double> t;
+    const double* dt = t45;
+    if (mem != COMBO_MEM_DEVICE) {
+      t.alloc(size_t(45 * c->N));
+      COMBO_CK(cudaMemcpyAsync(t.p, t45, size_t(45 * c->N) * 8, cudaMemcpyHostToDevice, c->stream));
+      dt = t.p;
+    }
+    const double* xx = stage_in(c, x, mem, 1);
+    double* yy = stage_out(c, y, mem, 2);
+    k_t45_matvec<<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(dt, xx, yy, c->N);
+    ++c->launches;
+    COMBO_CK(cudaGetLastError());
+    finish_out(c, y, yy, mem, size_t(9 * c->N));
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int combo_project(combo_ctx* c, int kind, const double* in, double* out, int mem) {
+  return guarded(c, [&] {
+    if (!c->has_grid) throw ComboError(COMBO_ERR_STATE, "no grid (combo_set_grid)");
+    ensure_scratch(c);
+    const double* src = stage_in(c, in, mem, 0);
+    double* dst = stage_out(c, out, mem, 1);
+    project_fused(c, kind, ProdLoad9{src, c->N}, ConsStore9{dst, c->N}, 0, 0);
+    finish_out(c, out, dst, mem, size_t(9 * c->N));
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int combo_fft_forward(combo_ctx* c, const int64_t dims[3], int ncomp, const double* in, double* out, int mem) {
+  return guarded(c, [&] {
+    if (ncomp < 1 || ncomp > 9) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ncomp must be 1..9");
+    double L[3] = {1, 1, 1};
+    if (c->has_grid) std::memcpy(L, c->lengths.data(), sizeof L);
+    set_grid(c, dims, L);
+    ensure_scratch(c);
+    const int64_t N = c->N;
+    c->scratch[0].alloc(size_t(9 * N));
+    COMBO_CK(cudaMemsetAsync(c->scratch[0].p, 0, size_t(9 * N) * 8, c->stream));
+    COMBO_CK(cudaMemcpyAsync(c->scratch[0].p, in, size_t(ncomp * N) * 8,
+                             mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    FftPlan& p = *c->plan;
+    launch_zfwd(c, ProdLoad9{c->scratch[0].p, N});
+    launch_y<false>(c);
+    launch_x_plain<false>(c);
+    // unpadded interleaved copy out
+    const size_t rows = size_t(ncomp * p.dims[0] * p.dims[1]);
+    COMBO_CK(cudaMemcpy2DAsync(out, size_t(p.n3c) * 16, p.spec.p, size_t(p.n3p) * 16, size_t(p.n3c) * 16, rows,
+                               mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int combo_solve(combo_ctx* c, const double fbar[9], const combo_solver_cfg* cfg, double* F_out, double* P_out,
+                double pbar[9], combo_report** report, int mem) {
+  return guarded(c, [&] {
+    require_bound(c);
+    if (!cfg || !fbar) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
+    // SolverConfig::validate (solver.cpp:277-284) + det check (:288-290)
+    if (cfg->eval == COMBO_EVAL_DFMG && cfg->green != COMBO_GREEN_STAGGERED)
+      throw ComboError(COMBO_ERR_CONFIG_INVALID,
+                       "solver: dfmg material evaluation requires the staggered Green operator");
+    if (cfg->load_steps < 1) throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: load_steps must be >= 1");
+    if (!(cfg->tol_equilibrium > 0.0))
+      throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: tol_equilibrium must be positive");
+    if (cfg->eval == COMBO_EVAL_DFMG)
+      throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: dfmg evaluation not available in this build");
+    if (!(hdet3(fbar) > 0.0)) throw ComboError(COMBO_ERR_INADMISSIBLE_MACRO, "solve: det(fbar) <= 0");
+    auto rep = std::make_unique<combo_report>();
+    Solver s(c, *cfg);
+    s.run(fbar, *rep);
+    if (pbar) std::memcpy(pbar, s.pbar(), 9 * sizeof(double));
+    if (P_out) {
+      double* p = mem == COMBO_MEM_DEVICE ? P_out : s.bufs_[6].p;
+      s.final_stress(p);
+      finish_out(c, P_out, p, mem, size_t(9 * c->N));
+    }
+    if (F_out) {
+      s.materialize();
+      if (mem == COMBO_MEM_DEVICE)
+        COMBO_CK(cudaMemcpyAsync(F_out, s.F(), size_t(9 * c->N) * 8, cudaMemcpyDeviceToDevice, c->stream));
+      else
+        COMBO_CK(cudaMemcpyAsync(F_out, s.F(), size_t(9 * c->N) * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+    rep->json = report_json(*rep);
+    if (report)
+      *report = rep.release();
+  });
+}
+
+int combo_report_summary(const combo_report* r, int* success, int* bisections, int* nsteps, double* alpha,
+                         double* seconds_total, int64_t* ls_total) {
+  if (!r) return COMBO_ERR_BAD_ARGUMENT;
+  if (success) *success = r->success ? 1 : 0;
+  if (bisections) *bisections = r->bisections;
+  if (nsteps) *nsteps = int(r->steps.size());
+  if (alpha) *alpha = r->alpha;
+  if (seconds_total) *seconds_total = r->seconds_total;
+  if (ls_total) *ls_total = r->ls_total;
+  return COMBO_OK;
+}
+
+int combo_report_step(const combo_report* r, int step, combo_step_info* info) {
+  if (!r || !info || step < 0 || size_t(step) >= r->steps.size()) return COMBO_ERR_BAD_ARGUMENT;
+  const auto& s = r->steps[size_t(step)];
+  info->t_start = s.t_start;
+  info->t_end = s.t_end;
+  std::memcpy(info->fbar, s.fbar, sizeof s.fbar);
+  info->converged = s.converged ? 1 : 0;
+  info->outer_iters = s.outer_iters;
+  info->cg_breakdowns = s.cg_breakdowns;
+  info->line_search_cuts = s.line_search_cuts;
+  info->n_residuals = int(s.residuals.size());
+  info->sweep = s.sweep;
+  info->seconds = s.seconds;
+  info->ls_basic = s.ls_basic;
+  info->ls_residual = s.ls_residual;
+  info->ls_cg = s.ls_cg;
+  info->ls_trial = s.ls_trial;
+  return COMBO_OK;
+}
+
+int combo_report_step_history(const combo_report* r, int step, double* residuals, double* pbar9, int* cg_iters) {
+  if (!r || step < 0 || size_t(step) >= r->steps.size()) return COMBO_ERR_BAD_ARGUMENT;
+  const auto& s = r->steps[size_t(step)];
+  for (size_t i = 0; i < s.residuals.size(); ++i) {
+    if (residuals) residuals[i] = s.residuals[i];
+    if (pbar9 && i < s.pbar_history.size()) std::memcpy(pbar9 + 9 * i, s.pbar_history[i].data(), 72);
+  }
+  if (cg_iters)
+    for (size_t i = 0; i < s.cg_iters.size(); ++i) cg_iters[i] = s.cg_iters[i];
+  return COMBO_OK;
+}
+
+const char* combo_report_json(const combo_report* r) { return r ? r->json.c_str() : "{}"; }
+
+int combo_report_free(combo_report* r) {
+  delete r;
+  return COMBO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,374 @@
+// Pointwise kernels of the LS iteration and the FFT producer/consumer
+// functors that fuse the solver updates into the first / last FFT pass.
+//
+// Reference loops replaced (file:line in /root/reference/proj/src):
+//   stress_sweep            cell_material.cpp:104-168   -> k_sweep
+//   tangent_matvec + p-upd. cell_material.cpp:170-194,
+//                           solver.cpp:194-197          -> k_matvec (matrix free)
+//   F update + residual     solver.cpp:135-149          -> ConsBasic (Z-inverse)
+//   b = -Pi(P), rms         solver.cpp:209-225          -> ConsResid
+//   pap = dot(pdir, Pi(q))  solver.cpp:180-181          -> ConsCg
+//   x += s p, r -= s ap, rr solver.cpp:186-190          -> k_cg_update
+//   ftrial = F + s x, mean  solver.cpp:241-243          -> k_trial
+//   Field9::mean / pin_mean field.cpp:18-38             -> k_sum9 / lazy shift
+#pragma once
+
+#include "fft.cuh"
+#include "material.cuh"
+
+namespace combo_dev {
+
+constexpr int kEwThreads = 256;
+
+// cid encoding: -1 pure matrix, -2 pure inclusion, >= 0 composite id
+struct CellData {
+  const int32_t* cid;
+  const double* nrm;  // [3][ncomp]
+  const double* cp;   // [ncomp]
+  const double* cm;   // [ncomp]
+  double* warm;       // [3][ncomp]
+  int64_t ncomp;
+};
+
+struct Stats {  // device counters (SweepStats)
+  unsigned long long inadmissible, failures, backproj, iter_max;
+};
+
+__device__ __forceinline__ void warp_stats(Stats* st, unsigned long long inad, unsigned long long fail,
+                                           unsigned long long bp, unsigned int itmax) {
+  const unsigned mask = __activemask();
+  const unsigned a = __reduce_add_sync(mask, unsigned(inad));
+  const unsigned f = __reduce_add_sync(mask, unsigned(fail));
+  const unsigned b = __reduce_add_sync(mask, unsigned(bp));
+  const unsigned m = __reduce_max_sync(mask, itmax);
+  if ((threadIdx.x & 31) == __ffs(mask) - 1) {
+    if (a) atomicAdd(&st->inadmissible, (unsigned long long)a);
+    if (f) atomicAdd(&st->failures, (unsigned long long)f);
+    if (b) atomicAdd(&st->backproj, (unsigned long long)b);
+    if (m) atomicMax(&st->iter_max, (unsigned long long)m);
+  }
+}
+
+// P(F) for one cell; returns false when inadmissible. Writes back the warm
+// start of composite cells when `writeback`.
+__device__ __forceinline__ bool cell_stress(const MatParams& M, const CellData& cd, int64_t cell,
+                                            const double* f, double* p, bool writeback, unsigned long long& fail,
+                                            unsigned long long& bp, unsigned int& itmax) {
+  const int32_t id = cd.cid[cell];
+  if (id >= 0) {
+    const double n[3] = {cd.nrm[id], cd.nrm[cd.ncomp + id], cd.nrm[2 * cd.ncomp + id]};
+    const double a0[3] = {cd.warm[id], cd.warm[cd.ncomp + id], cd.warm[2 * cd.ncomp + id]};
+    LamResult R;
+    laminate_solve(M, f, n, cd.cp[id], cd.cm[id], a0, R);
+    if (R.inadmissible) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) p[c] = 0.0;
+      return false;
+    }
+    if (!R.converged) ++fail;
+    bp += (unsigned long long)R.back_projections;
+    itmax = max(itmax, (unsigned)R.iterations);
+    if (writeback) {
+      cd.warm[id] = R.a[0];
+      cd.warm[cd.ncomp + id] = R.a[1];
+      cd.warm[2 * cd.ncomp + id] = R.a[2];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) p[c] = R.p[c];
+    return true;
+  }
+  NhState s;
+  const LawP L = id == -2 ? M.law[1] : M.law[0];
+  if (!law_eval(L, f, p, s)) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) p[c] = 0.0;
+    return false;
+  }
+  return true;
+}
+
+struct Shift9 {
+  double v[9];
+};
+
+// out = P(F_in + shift) - alpha (F_in + shift); partial sums of P (P-bar).
+static __global__ void __launch_bounds__(kEwThreads) k_sweep(MatParams M, CellData cd, const double* __restrict__ fin,
+                                                      Shift9 sh, double alpha, double* __restrict__ out,
+                                                      int64_t N, int writeback, Stats* st, double* partials) {
+  double acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0.0;
+  unsigned long long inad = 0, fail = 0, bp = 0;
+  unsigned int itmax = 0;
+  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
+       cell += int64_t(gridDim.x) * blockDim.x) {
+    double f[9], p[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell] + sh.v[c];
+    if (!cell_stress(M, cd, cell, f, p, writeback != 0, fail, bp, itmax)) ++inad;
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      acc[c] += p[c];
+      out[c * N + cell] = alpha != 0.0 ? p[c] + (-alpha) * f[c] : p[c];
+    }
+  }
+  warp_stats(st, inad, fail, bp, itmax);
+  block_reduce_store<9>(acc, partials, blockIdx.x);
+}
+
+// pdir = first ? r : r + beta * pdir ; q = A(F) : pdir   (matrix free)
+static __global__ void __launch_bounds__(kEwThreads) k_matvec(MatParams M, CellData cd, const double* __restrict__ fin,
+                                                       Shift9 sh, const double* __restrict__ r, double* pdir,
+                                                       double beta, int first, double* __restrict__ q,
+                                                       int64_t N) {
+  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
+       cell += int64_t(gridDim.x) * blockDim.x) {
+    double f[9], x[9], y[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      const double rv = r[c * N + cell];
+      x[c] = first ? rv : rv + beta * pdir[c * N + cell];
+      f[c] = fin[c * N + cell] + sh.v[c];
+    }
+    if (!first || pdir != r) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) pdir[c * N + cell] = x[c];
+    }
+    const int32_t id = cd.cid[cell];
+    if (id >= 0) {
+      const double n[3] = {cd.nrm[id], cd.nrm[cd.ncomp + id], cd.nrm[2 * cd.ncomp + id]};
+      const double a[3] = {cd.warm[id], cd.warm[cd.ncomp + id], cd.warm[2 * cd.ncomp + id]};
+      if (det3(f) > 0.0)
+        laminate_apply(M, f, n, cd.cp[id], cd.cm[id], a, x, y);
+      else
+        for (int c = 0; c < 9; ++c) y[c] = x[c];
+    } else {
+      const LawP L = id == -2 ? M.law[1] : M.law[0];
+      NhState s;
+      double p[9];
+      if (law_eval(L, f, p, s))
+        law_apply(L, s, x, y);
+      else
+        for (int c = 0; c < 9; ++c) y[c] = x[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) q[c * N + cell] = y[c];
+  }
+}
+
+// Flat 9N update: x += step * p ; r -= step * ap ; partial sum of r^2
+static __global__ void __launch_bounds__(kEwThreads) k_cg_update(double* __restrict__ x, double* __restrict__ r,
+                                                          const double* __restrict__ p,
+                                                          const double* __restrict__ ap, double step,
+                                                          int64_t n, double* partials) {
+  double acc[1] = {0.0};
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    x[i] += step * p[i];
+    const double rv = r[i] + (-step) * ap[i];
+    r[i] = rv;
+    acc[0] += rv * rv;
+  }
+  block_reduce_store<1>(acc, partials, blockIdx.x);
+}
+
+// ftrial = (F + shiftF) + s x ; per-component sums for pin_mean
+static __global__ void __launch_bounds__(kEwThreads) k_trial(const double* __restrict__ f, Shift9 sh,
+                                                      const double* __restrict__ x, double s,
+                                                      double* __restrict__ ft, int64_t N, double* partials) {
+  double acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0.0;
+  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
+       cell += int64_t(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      const double v = (f[c * N + cell] + sh.v[c]) + s * x[c * N + cell];
+      ft[c * N + cell] = v;
+      acc[c] += v;
+    }
+  }
+  block_reduce_store<9>(acc, partials, blockIdx.x);
+}
+
+// f = f + shift (materialize), per-component sums of the result
+static __global__ void __launch_bounds__(kEwThreads) k_materialize(double* __restrict__ f, Shift9 sh, int64_t N,
+                                                            double* partials) {
+  double acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0.0;
+  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
+       cell += int64_t(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      const double v = f[c * N + cell] + sh.v[c];
+      f[c * N + cell] = v;
+      acc[c] += v;
+    }
+  }
+  block_reduce_store<9>(acc, partials, blockIdx.x);
+}
+
+static __global__ void k_fill9(double* f, Shift9 val, int64_t N) {
+  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
+       cell += int64_t(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) f[c * N + cell] = val.v[c];
+  }
+}
+
+// y_cell = A x_cell with packed 45 tangents (API compatibility path)
+static __global__ void k_t45_matvec(const double* __restrict__ t45, const double* __restrict__ x, double* __restrict__ y,
+                             int64_t N) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += int64_t(gridDim.x) * blockDim.x) {
+    const double* a = t45 + 45 * i;
+    double xv[9], yv[9];
+    for (int c = 0; c < 9; ++c) {
+      xv[c] = x[c * N + i];
+      yv[c] = 0.0;
+    }
+    int t = 0;
+    for (int r = 0; r < 9; ++r) {
+      yv[r] += a[t] * xv[r];
+      ++t;
+      for (int c = r + 1; c < 9; ++c, ++t) {
+        yv[r] += a[t] * xv[c];
+        yv[c] += a[t] * xv[r];
+      }
+    }
+    for (int c = 0; c < 9; ++c) y[c * N + i] = yv[c];
+  }
+}
+
+// packed tangent = columns of A applied to unit vectors (matrix free), sym.
+static __global__ void k_tangent45(MatParams M, CellData cd, const double* __restrict__ fin, double* __restrict__ t45,
+                            int64_t N) {
+  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
+       cell += int64_t(gridDim.x) * blockDim.x) {
+    double f[9];
+    for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell];
+    double A[81];
+    const int32_t id = cd.cid[cell];
+    for (int col = 0; col < 9; ++col) {
+      double x[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, y[9];
+      x[col] = 1.0;
+      if (id >= 0) {
+        const double n[3] = {cd.nrm[id], cd.nrm[cd.ncomp + id], cd.nrm[2 * cd.ncomp + id]};
+        const double a[3] = {cd.warm[id], cd.warm[cd.ncomp + id], cd.warm[2 * cd.ncomp + id]};
+        if (det3(f) > 0.0)
+          laminate_apply(M, f, n, cd.cp[id], cd.cm[id], a, x, y);
+        else
+          for (int c = 0; c < 9; ++c) y[c] = x[c];
+      } else {
+        const LawP L = id == -2 ? M.law[1] : M.law[0];
+        NhState s;
+        double p[9];
+        if (law_eval(L, f, p, s))
+          law_apply(L, s, x, y);
+        else
+          for (int c = 0; c < 9; ++c) y[c] = x[c];
+      }
+      for (int r = 0; r < 9; ++r) A[9 * r + col] = y[r];
+    }
+    int t = 0;
+    for (int r = 0; r < 9; ++r)
+      for (int c = r; c < 9; ++c) t45[45 * cell + (t++)] = 0.5 * (A[9 * r + c] + A[9 * c + r]);
+  }
+}
+
+// Deterministic final reduction: one block per value, fixed strided
+// assignment + fixed tree.
+static __global__ void k_reduce_partials(const double* __restrict__ partials, int64_t nblocks, int nred,
+                                  double* __restrict__ out) {
+  __shared__ double sm[1024];
+  const int r = blockIdx.x;
+  double s = 0.0;
+  for (int64_t b = threadIdx.x; b < nblocks; b += blockDim.x) s += partials[b * nred + r];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x >> 1; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[r] = sm[0];
+}
+
+// ------------------------------------------------------------ FFT functors
+// FIELDS = real 9N-field streams (reads + writes) besides the spectrum; used
+// for the algorithmic-bytes bookkeeping of the profiler.
+struct ProdLoad9 {
+  static constexpr int NRED = 0;
+  static constexpr int FIELDS = 1;
+  const double* src;
+  int64_t N;
+  __device__ __forceinline__ void operator()(int64_t cell, double* v, double*) const {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) v[c] = src[c * N + cell];
+  }
+};
+
+struct ConsStore9 {
+  static constexpr int NRED = 0;
+  static constexpr int FIELDS = 1;
+  double* dst;
+  int64_t N;
+  __device__ __forceinline__ void operator()(int64_t cell, const double* v, double*) const {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) dst[c * N + cell] = v[c];
+  }
+};
+
+// run_basic F update (solver.cpp:135-149): F_new = fbar - Pi(tau)/alpha,
+// diff against the pinned F_old; sums of diff^2 and of F_new.
+struct ConsBasic {
+  static constexpr int NRED = 10;
+  static constexpr int FIELDS = 2;
+  const double* fold;
+  Shift9 fold_shift;
+  double* fnew;
+  Shift9 fbar;
+  double alpha;
+  int64_t N;
+  __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      const double fn = fbar.v[c] - v[c] / alpha;
+      const double d = fn - (fold[c * N + cell] + fold_shift.v[c]);
+      acc[0] += d * d;
+      acc[1 + c] += fn;
+      fnew[c * N + cell] = fn;
+    }
+  }
+};
+
+// Newton residual (solver.cpp:209-225): r = -Pi(P), sum of Pi(P)^2
+struct ConsResid {
+  static constexpr int NRED = 1;
+  static constexpr int FIELDS = 1;
+  double* r;
+  int64_t N;
+  __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      r[c * N + cell] = -v[c];
+      acc[0] += v[c] * v[c];
+    }
+  }
+};
+
+// CG (solver.cpp:180-181): ap = Pi(q), sum of pdir . ap
+struct ConsCg {
+  static constexpr int NRED = 1;
+  static constexpr int FIELDS = 2;
+  double* ap;
+  const double* pdir;
+  int64_t N;
+  __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      ap[c * N + cell] = v[c];
+      acc[0] += pdir[c * N + cell] * v[c];
+    }
+  }
+};
+
+}  // namespace combo_dev
