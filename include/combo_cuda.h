@@ -179,6 +179,10 @@ int combo_stress_floor(const combo_ctx* ctx, double* floor);
 /* warm starts (jump vectors) per composite id, 3 doubles each */
 int combo_get_warm_starts(combo_ctx* ctx, double* warm3, int mem);
 int combo_set_warm_starts(combo_ctx* ctx, const double* warm3, int mem);
+/* CellMaterials::reset_warm_starts (cell_material.cpp:64-66) */
+int combo_reset_warm_starts(combo_ctx* ctx);
+/* the cudaStream_t all of ctx's kernels run on (for external CUDA events) */
+int combo_get_stream(combo_ctx* ctx, void** stream);
 int combo_spectrum_bounds(combo_ctx* ctx, const double fbar[9], double* lo, double* hi);
 
 /* --------------------------------------------------------------- operators */

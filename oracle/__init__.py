@@ -130,7 +130,8 @@ def lam_opts(tol_abs=0.0, tol_rel=1e-10, stress_floor=0.0, max_iter=50, back_pro
 
 
 # ------------------------------------------------------------ generators
-SHAPES = {"sphere": 0, "octahedron": 1, "fiber": 2, "cross_ply": 3, "fiber_pack": 4, "slab": 5}
+SHAPES = {"sphere": 0, "octahedron": 1, "fiber": 2, "cross_ply": 3, "fiber_pack": 4, "slab": 5,
+          "rsa_spheres": 10, "rsa_fibers_z": 11, "boolean_ellipsoids": 12}
 
 
 def generate(shape, dims, lengths=(1.0, 1.0, 1.0), *params):

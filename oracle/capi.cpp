@@ -98,6 +98,9 @@ int oracle_generate(int shape, const std::int64_t* dims, const double* lengths,
                                   params[3], params[4]);
         break;
       case 5: img = generate_slab(d, l, int(params[0]), params[1]); break;
+      case 10:
+      case 11:
+      case 12: img = generate_config(shape, d, l, params); break;
       default: g_err = "unknown shape"; return -13;
     }
     std::memcpy(out, img.data.data(), img.data.size());

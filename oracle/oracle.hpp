@@ -290,6 +290,10 @@ PhaseImage generate_slab(const std::array<std::int64_t, 3>& dims,
                          const std::array<double, 3>& lengths, int axis,
                          double fraction);
 PhaseImage mirrored(const PhaseImage& img, int axis);
+/// seeded config microstructures (shape 10 rsa spheres, 11 rsa z-fibres,
+/// 12 Boolean ellipsoids); see preprocess.cpp
+PhaseImage generate_config(int shape, const std::array<std::int64_t, 3>& dims,
+                           const std::array<double, 3>& lengths, const double* params);
 
 enum BoxelKind : std::uint8_t { kPureMatrix = 0, kPureInclusion = 1, kComposite = 2 };
 enum NormalFlag : std::uint8_t {

@@ -194,6 +194,163 @@ PhaseImage mirrored(const PhaseImage& img, int axis) {
   return out;
 }
 
+// ------------------------------------------------ seeded config generators
+// The BASELINE configs' microstructures do not exist in the reference
+// (SURVEY.md §8d). This restates the product's generators (random sequential
+// addition of periodic spheres / z-disks, Boolean ellipsoids; splitmix64 as
+// image.cpp:18-32) on the CPU with the same draw order and the same voxel
+// predicates, so both arms see bit-identical images.
+namespace {
+struct Obj {
+  double c[3], a[3], R[9], r;
+  int type;  // 0 sphere, 1 z-cylinder, 2 ellipsoid
+};
+
+std::vector<Obj> rsa_objects(const std::array<double, 3>& L, double h, std::uint64_t seed, double rmin,
+                             double rmax, double phi, bool dim2) {
+  const double r_lo = rmin * h, r_hi = rmax * h;
+  const double target = dim2 ? phi * L[0] * L[1] : phi * L[0] * L[1] * L[2];
+  const double kPi = 3.141592653589793238462643383279502884;
+  Splitmix64 rng(seed);
+  const double cs = 2.0 * r_hi;
+  int nc[3];
+  for (int a = 0; a < 3; ++a) nc[a] = std::max(1, int(L[a] / cs));
+  if (dim2) nc[2] = 1;
+  std::vector<std::vector<int>> cells(std::size_t(nc[0]) * nc[1] * nc[2]);
+  std::vector<Obj> out;
+  double acc = 0.0;
+  for (std::int64_t att = 0; acc < target; ++att) {
+    if (att >= 200000000LL) throw BadShapeSpec("rsa: volume fraction not reachable");
+    Obj o{};
+    o.c[0] = rng.unit() * L[0];
+    o.c[1] = rng.unit() * L[1];
+    o.c[2] = dim2 ? 0.5 * L[2] : rng.unit() * L[2];
+    const double r = r_lo + (r_hi - r_lo) * rng.unit();
+    int ci[3];
+    for (int a = 0; a < 3; ++a) ci[a] = std::min(nc[a] - 1, int(o.c[a] / L[a] * nc[a]));
+    auto clash = [&](const Obj& q) {
+      const double ex = wrapd(o.c[0] - q.c[0], L[0]), ey = wrapd(o.c[1] - q.c[1], L[1]);
+      const double ez = dim2 ? 0.0 : wrapd(o.c[2] - q.c[2], L[2]);
+      const double rr = r + q.a[0];
+      return ex * ex + ey * ey + ez * ez < rr * rr;
+    };
+    bool ok = true;
+    if (nc[0] < 3 || nc[1] < 3 || (!dim2 && nc[2] < 3)) {
+      for (const Obj& q : out)
+        if (clash(q)) {
+          ok = false;
+          break;
+        }
+    } else {
+      for (int dx = -1; dx <= 1 && ok; ++dx)
+        for (int dy = -1; dy <= 1 && ok; ++dy)
+          for (int dz = (dim2 ? 0 : -1); dz <= (dim2 ? 0 : 1) && ok; ++dz) {
+            const int a = ((ci[0] + dx) % nc[0] + nc[0]) % nc[0];
+            const int b = ((ci[1] + dy) % nc[1] + nc[1]) % nc[1];
+            const int c = ((ci[2] + dz) % nc[2] + nc[2]) % nc[2];
+            for (int idx : cells[(std::size_t(a) * nc[1] + b) * nc[2] + c])
+              if (clash(out[std::size_t(idx)])) {
+                ok = false;
+                break;
+              }
+          }
+    }
+    if (!ok) continue;
+    o.type = dim2 ? 1 : 0;
+    o.a[0] = o.a[1] = o.a[2] = r;
+    o.r = r;
+    cells[(std::size_t(ci[0]) * nc[1] + ci[1]) * nc[2] + ci[2]].push_back(int(out.size()));
+    out.push_back(o);
+    acc += dim2 ? kPi * r * r : 4.0 / 3.0 * kPi * r * r * r;
+  }
+  return out;
+}
+
+std::vector<Obj> boolean_ellipsoid_objects(const std::array<double, 3>& L, double h, std::uint64_t seed,
+                                           double amin, double amax, double phi) {
+  const double kPi = 3.141592653589793238462643383279502884;
+  const double target = -std::log(1.0 - phi) * (L[0] * L[1] * L[2]);
+  Splitmix64 rng(seed);
+  std::vector<Obj> out;
+  double acc = 0.0;
+  while (acc < target) {
+    Obj o{};
+    for (int a = 0; a < 3; ++a) o.c[a] = rng.unit() * L[a];
+    for (int a = 0; a < 3; ++a) o.a[a] = h * (amin + (amax - amin) * rng.unit());
+    const double u1 = rng.unit(), u2 = rng.unit(), u3 = rng.unit();
+    const double s1 = std::sqrt(1.0 - u1), s2 = std::sqrt(u1);
+    const double qx = s1 * std::sin(2 * kPi * u2), qy = s1 * std::cos(2 * kPi * u2);
+    const double qz = s2 * std::sin(2 * kPi * u3), qw = s2 * std::cos(2 * kPi * u3);
+    const double R[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qz * qw),     2 * (qx * qz + qy * qw),
+                         2 * (qx * qy + qz * qw),     1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qx * qw),
+                         2 * (qx * qz - qy * qw),     2 * (qy * qz + qx * qw),     1 - 2 * (qx * qx + qy * qy)};
+    for (int i = 0; i < 9; ++i) o.R[i] = R[i];
+    o.r = std::max(o.a[0], std::max(o.a[1], o.a[2]));
+    o.type = 2;
+    out.push_back(o);
+    acc += 4.0 / 3.0 * kPi * o.a[0] * o.a[1] * o.a[2];
+  }
+  return out;
+}
+}  // namespace
+
+PhaseImage generate_config(int shape, const std::array<std::int64_t, 3>& dims, const std::array<double, 3>& L,
+                           const double* p) {
+  PhaseImage img;
+  img.dims = dims;
+  img.lengths = L;
+  img.data.assign(std::size_t(img.size()), 0);
+  const double h[3] = {L[0] / double(dims[0]), L[1] / double(dims[1]), L[2] / double(dims[2])};
+  std::vector<Obj> objs;
+  if (shape == 10) objs = rsa_objects(L, h[0], std::uint64_t(p[0]), p[1], p[2], p[3], false);
+  else if (shape == 11) objs = rsa_objects(L, h[0], std::uint64_t(p[0]), p[1], p[1], p[2], true);
+  else if (shape == 12) objs = boolean_ellipsoid_objects(L, h[0], std::uint64_t(p[0]), p[1], p[2], p[3]);
+  else throw BadShapeSpec("generate_config: unknown shape");
+  const auto n1 = dims[0], n2 = dims[1], n3 = dims[2];
+#pragma omp parallel for schedule(dynamic, 64)
+  for (std::int64_t o = 0; o < std::int64_t(objs.size()); ++o) {
+    const Obj& ob = objs[std::size_t(o)];
+    const std::int64_t i0 = std::int64_t(std::floor((ob.c[0] - ob.r) / h[0])) - 1;
+    const std::int64_t i1 = std::int64_t(std::floor((ob.c[0] + ob.r) / h[0])) + 1;
+    const std::int64_t j0 = std::int64_t(std::floor((ob.c[1] - ob.r) / h[1])) - 1;
+    const std::int64_t j1 = std::int64_t(std::floor((ob.c[1] + ob.r) / h[1])) + 1;
+    std::int64_t k0 = std::int64_t(std::floor((ob.c[2] - ob.r) / h[2])) - 1;
+    std::int64_t k1 = std::int64_t(std::floor((ob.c[2] + ob.r) / h[2])) + 1;
+    if (ob.type == 1) {
+      k0 = 0;
+      k1 = n3 - 1;
+    }
+    const std::int64_t ni = std::min(i1 - i0 + 1, n1), nj = std::min(j1 - j0 + 1, n2), nk = std::min(k1 - k0 + 1, n3);
+    for (std::int64_t ii = 0; ii < ni; ++ii)
+      for (std::int64_t jj = 0; jj < nj; ++jj)
+        for (std::int64_t kk = 0; kk < nk; ++kk) {
+          const std::int64_t i = wrapi(i0 + ii, n1), j = wrapi(j0 + jj, n2), k = wrapi(k0 + kk, n3);
+          const double x = (double(i) + 0.5) * h[0], y = (double(j) + 0.5) * h[1], z = (double(k) + 0.5) * h[2];
+          const double dx = wrapd(x - ob.c[0], L[0]), dy = wrapd(y - ob.c[1], L[1]), dz = wrapd(z - ob.c[2], L[2]);
+          bool in;
+          if (ob.type == 0) {
+            in = dx * dx + dy * dy + dz * dz < ob.a[0] * ob.a[0];
+          } else if (ob.type == 1) {
+            in = dx * dx + dy * dy < ob.a[0] * ob.a[0];
+          } else {
+            const double b0 = ob.R[0] * dx + ob.R[3] * dy + ob.R[6] * dz;
+            const double b1 = ob.R[1] * dx + ob.R[4] * dy + ob.R[7] * dz;
+            const double b2 = ob.R[2] * dx + ob.R[5] * dy + ob.R[8] * dz;
+            const double q = (b0 / ob.a[0]) * (b0 / ob.a[0]) + (b1 / ob.a[1]) * (b1 / ob.a[1]) +
+                             (b2 / ob.a[2]) * (b2 / ob.a[2]);
+            in = q < 1.0;
+          }
+          if (in) {
+            // idempotent byte store; objects may overlap (Boolean model)
+            std::uint8_t* px = &img.data[std::size_t((i * n2 + j) * n3 + k)];
+#pragma omp atomic write
+            *px = 1;
+          }
+        }
+  }
+  return img;
+}
+
 // ---------------------------------------------------------------- coarsen
 std::int64_t ComboGrid::composite_count() const {
   std::int64_t n = 0;

@@ -82,6 +82,10 @@ SIGNATURES = {
     "combo_version": (C.c_char_p, []),
     "combo_kernel_launches": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
     "combo_synchronize": (C.c_int, [_VP]),
+    "combo_profile_enable": (C.c_int, [_VP, C.c_int]),
+    "combo_profile_json": (C.c_char_p, [_VP]),
+    "combo_reset_warm_starts": (C.c_int, [_VP]),
+    "combo_get_stream": (C.c_int, [_VP, C.POINTER(C.c_void_p)]),
     "combo_generate": (C.c_int, [_VP, C.c_int, _I64, _D, _D, C.c_int, _VP, C.c_int]),
     "combo_coarsen": (C.c_int, [_VP, _VP, _I64, _I64, _VP, _VP, _VP, C.c_int]),
     "combo_laplace_weights": (C.c_int, [_VP, _VP, _I64, _D, _VP, C.c_int]),
@@ -131,12 +135,25 @@ def load_library(path=None):
     return _LIB
 
 
+def _is_dev(a):
+    return hasattr(a, "data_ptr") and getattr(a, "is_cuda", False)
+
+
 def _ptr(a):
     if a is None:
         return None
     if isinstance(a, int):
         return C.c_void_p(a)
+    if hasattr(a, "data_ptr"):  # torch tensor (device memory or pinned host)
+        return C.c_void_p(a.data_ptr())
     return a.ctypes.data_as(C.c_void_p)
+
+
+def _mem(*arrays):
+    dev = [_is_dev(a) for a in arrays if a is not None]
+    if any(dev) and not all(dev):
+        raise ComboError(-13, "mixing host and device arrays in one call")
+    return MEM_DEVICE if dev and dev[0] else MEM_HOST
 
 
 def neo_hookean(lam, mu):
@@ -239,26 +256,55 @@ class Context:
         self._check(self.L.combo_kernel_launches(self.h, C.byref(v)))
         return int(v.value)
 
+    @property
+    def stream(self):
+        s = C.c_void_p()
+        self._check(self.L.combo_get_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self):
+        self._check(self.L.combo_synchronize(self.h))
+
+    def profile(self, enable=True):
+        self._check(self.L.combo_profile_enable(self.h, int(enable)))
+
+    def profile_report(self):
+        return json.loads(self.L.combo_profile_json(self.h).decode())
+
     # ------------------------------------------------------------ images
-    def generate(self, shape, dims, lengths=(1.0, 1.0, 1.0), *params):
+    def generate(self, shape, dims, lengths=(1.0, 1.0, 1.0), *params, out=None):
+        """generate_* (image.cpp:57-227) and the seeded config generators;
+        `out` may be a CUDA uint8 tensor (device result)."""
         ids = {"sphere": 0, "octahedron": 1, "slab": 5, "rsa_spheres": 10, "rsa_fibers_z": 11,
                "boolean_ellipsoids": 12}
-        out = np.zeros(int(np.prod(dims)), dtype=np.uint8)
+        if out is None:
+            out = np.zeros(int(np.prod(dims)), dtype=np.uint8)
         p = _f64(list(params) + [0.0] * (8 - len(params)))
         self._check(self.L.combo_generate(self.h, ids[shape], _i64(dims), _f64(lengths), p, len(params),
-                                          _ptr(out), MEM_HOST))
+                                          _ptr(out), _mem(out)))
         return out.reshape(tuple(dims))
 
-    def coarsen(self, img, factors):
-        """coarsen (combo_grid.cpp:28-71) -> kind, c_plus, count_plus"""
-        img = np.ascontiguousarray(img, dtype=np.uint8)
-        dims = _i64(img.shape)
-        f = _i64(factors)
-        nb = int(np.prod(dims // np.maximum(f, 1)))
-        kind = np.zeros(nb, np.uint8)
-        cp = np.zeros(nb)
-        cnt = np.zeros(nb, np.int64)
-        self._check(self.L.combo_coarsen(self.h, _ptr(img), dims, f, _ptr(kind), _ptr(cp), _ptr(cnt), MEM_HOST))
+    def coarsen(self, img, factors, dims=None):
+        """coarsen (combo_grid.cpp:28-71) -> kind, c_plus, count_plus (device
+        tensors when img is a CUDA tensor)"""
+        if _is_dev(img):
+            import torch
+
+            dims = _i64(dims if dims is not None else img.shape)
+            f = _i64(factors)
+            nb = int(np.prod(dims // np.maximum(f, 1)))
+            kind = torch.empty(nb, dtype=torch.uint8, device=img.device)
+            cp = torch.empty(nb, dtype=torch.float64, device=img.device)
+            cnt = torch.empty(nb, dtype=torch.int64, device=img.device)
+        else:
+            img = np.ascontiguousarray(img, dtype=np.uint8)
+            dims = _i64(img.shape)
+            f = _i64(factors)
+            nb = int(np.prod(dims // np.maximum(f, 1)))
+            kind = np.zeros(nb, np.uint8)
+            cp = np.zeros(nb)
+            cnt = np.zeros(nb, np.int64)
+        self._check(self.L.combo_coarsen(self.h, _ptr(img), dims, f, _ptr(kind), _ptr(cp), _ptr(cnt), _mem(img)))
         return kind, cp, cnt
 
     def laplace_weights(self, img, lengths=(1.0, 1.0, 1.0)):
@@ -269,19 +315,28 @@ class Context:
         return w.reshape(img.shape)
 
     def compute_normals(self, img, factors, kind, lengths=(1.0, 1.0, 1.0), method="second_moment",
-                        centering="weighted_centroid", min_interface_voxels=3):
+                        centering="weighted_centroid", min_interface_voxels=3, dims=None):
         """compute_normals (normals.cpp:211-256) -> normals (nb,3), flags, stats"""
-        img = np.ascontiguousarray(img, dtype=np.uint8)
-        kind = np.ascontiguousarray(kind, dtype=np.uint8)
-        nb = kind.size
-        n3 = np.zeros(3 * nb)
-        flags = np.zeros(nb, np.uint8)
+        if _is_dev(img):
+            import torch
+
+            dims = dims if dims is not None else img.shape
+            nb = kind.numel()
+            n3 = torch.empty(3 * nb, dtype=torch.float64, device=img.device)
+            flags = torch.empty(nb, dtype=torch.uint8, device=img.device)
+        else:
+            img = np.ascontiguousarray(img, dtype=np.uint8)
+            dims = img.shape
+            kind = np.ascontiguousarray(kind, dtype=np.uint8)
+            nb = kind.size
+            n3 = np.zeros(3 * nb)
+            flags = np.zeros(nb, np.uint8)
         st = NormalStats()
         m = {"barycenter": 0, "second_moment": 1}[method]
         cen = {"weighted_centroid": 0, "boxel_center": 1}[centering]
-        self._check(self.L.combo_normals(self.h, _ptr(img), _i64(img.shape), _f64(lengths), _i64(factors),
+        self._check(self.L.combo_normals(self.h, _ptr(img), _i64(dims), _f64(lengths), _i64(factors),
                                          _ptr(kind), m, cen, int(min_interface_voxels), _ptr(n3), _ptr(flags),
-                                         C.byref(st), MEM_HOST))
+                                         C.byref(st), _mem(img, kind)))
         return n3.reshape(nb, 3), flags, (st.composite, st.degenerate_fallbacks, st.too_few_fallbacks)
 
     # --------------------------------------------------------- operators
@@ -328,13 +383,18 @@ class CellMaterials:
         self.dims = tuple(int(d) for d in dims)
         self.lengths = tuple(float(x) for x in lengths)
         self.n = int(np.prod(self.dims))
-        kind = np.ascontiguousarray(kind, dtype=np.uint8).ravel()
-        cp = _f64(c_plus).ravel()
-        nrm = None if normal is None else _f64(normal).ravel()
+        if not _is_dev(kind):
+            kind = np.ascontiguousarray(kind, dtype=np.uint8).ravel()
+            c_plus = _f64(c_plus).ravel()
+            normal = None if normal is None else _f64(normal).ravel()
         oc = (opts or LaminateOptions()).c()
-        ctx._check(ctx.L.combo_bind_materials(ctx.h, _i64(self.dims), _f64(self.lengths), _ptr(kind), _ptr(cp),
-                                              _ptr(nrm), C.byref(matrix), C.byref(inclusion), int(combo),
-                                              C.byref(oc), MEM_HOST))
+        ctx._check(ctx.L.combo_bind_materials(ctx.h, _i64(self.dims), _f64(self.lengths), _ptr(kind),
+                                              _ptr(c_plus), _ptr(normal), C.byref(matrix), C.byref(inclusion),
+                                              int(combo), C.byref(oc), _mem(kind, c_plus, normal)))
+
+    def reset_warm_starts(self):
+        """CellMaterials::reset_warm_starts (cell_material.cpp:64-66)"""
+        self.ctx._check(self.ctx.L.combo_reset_warm_starts(self.ctx.h))
 
     @property
     def composites(self):
@@ -387,17 +447,18 @@ class CellMaterials:
                                                              _ptr(_f64(x).ravel()), _ptr(y), MEM_HOST))
         return y
 
-    def solve(self, fbar, cfg=None, want_fields=True, **kw):
-        """solve (solver.cpp:286-346) -> dict(f, p, pbar, report)"""
+    def solve(self, fbar, cfg=None, want_fields=True, f_out=None, p_out=None, **kw):
+        """solve (solver.cpp:286-346) -> dict(f, p, pbar, report). f_out /
+        p_out may be caller buffers (numpy / pinned or CUDA tensors)."""
         cfg = cfg or SolverConfig(**kw)
-        F = np.zeros(9 * self.n) if want_fields else None
-        P = np.zeros(9 * self.n) if want_fields else None
+        F = f_out if f_out is not None else (np.zeros(9 * self.n) if want_fields else None)
+        P = p_out if p_out is not None else (np.zeros(9 * self.n) if want_fields else None)
         pbar = np.zeros(9)
         rep = C.c_void_p()
         cc = cfg.c()
         L = self.ctx.L
         self.ctx._check(L.combo_solve(self.ctx.h, _f64(np.asarray(fbar).ravel()), C.byref(cc), _ptr(F), _ptr(P),
-                                      pbar, C.byref(rep), MEM_HOST))
+                                      pbar, C.byref(rep), _mem(F, P)))
         report = json.loads(L.combo_report_json(rep).decode())
         L.combo_report_free(rep)
         return dict(f=F, p=P, pbar=pbar.reshape(3, 3), report=report)

@@ -1217,6 +1217,21 @@ int combo_set_warm_starts(combo_ctx* c, const double* warm3, int mem) {
   });
 }
 
+int combo_reset_warm_starts(combo_ctx* c) {
+  return guarded(c, [&] {
+    require_bound(c);
+    if (c->ncomp) COMBO_CK(cudaMemsetAsync(c->warm.p, 0, size_t(3 * c->ncomp) * 8, c->stream));
+    if (c->dfmg_warm.p) COMBO_CK(cudaMemsetAsync(c->dfmg_warm.p, 0, c->dfmg_warm.n * 8, c->stream));
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int combo_get_stream(combo_ctx* c, void** stream) {
+  if (!c || !stream) return COMBO_ERR_BAD_ARGUMENT;
+  *stream = reinterpret_cast<void*>(c->stream);
+  return COMBO_OK;
+}
+
 int combo_stress_sweep(combo_ctx* c, const double* F, double* P, combo_sweep_stats* st, int mem) {
   return guarded(c, [&] {
     require_bound(c);
