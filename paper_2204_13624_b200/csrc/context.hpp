@@ -86,6 +86,10 @@ struct FftPlan {
   int yW = 8, yT = 32;           // y pass tile width, threads
   int xW = 8, xT = 32;           // x pass tile width (3 components per tile)
   size_t zsmem = 0, ysmem = 0, xsmem = 0;
+  // register-resident pow2 path (fft_rr.cuh), used when the axis length is
+  // a power of two >= 8
+  int rzL = 1, rzT = 32, ryW = 8, ryT = 32, rxW = 4, rxT = 32;
+  size_t rzsmem = 0, rysmem = 0, rxsmem = 0;
   DBuf<double2> spec;
   combo_dev::SpecView sv() const {
     combo_dev::SpecView s;
@@ -147,10 +151,14 @@ struct combo_ctx {
   double stress_floor = 1e-300;
   combo_host::DBuf<int32_t> cid;
   combo_host::DBuf<double> nrm, cp, cm, warm;
+  combo_host::DBuf<int64_t> ccell;  // composite id -> cell
+  combo_host::DBuf<double> t45;     // [45][ncomp] packed composite tangents
   int64_t ncomp = 0;
   combo_dev::MatParams mp{};
   combo_host::DBuf<double> a9;  // linear-law 9x9 tangents (device)
-  combo_host::DBuf<double> dfmg_warm;  // [3][8N] per doubly-fine cell
+  combo_host::DBuf<double> dfmg_warm;  // [3][8 ncomp] per doubly-fine cell of a composite host
+  combo_host::DBuf<double> dfmg_pd;    // [9][8][N] per-dfc stress / tangent products
+  combo_host::DBuf<double> dfmg_t8;    // [45][8 ncomp] per-dfc packed tangents
 
   // scratch
   combo_host::DBuf<double> partials;   // per-block partial sums
@@ -178,6 +186,8 @@ struct combo_ctx {
     c.cm = cm.p;
     c.warm = warm.p;
     c.ncomp = ncomp;
+    c.ccell = ccell.p;
+    c.t45 = t45.p;
     return c;
   }
 };
@@ -190,6 +200,12 @@ void ensure_scratch(combo_ctx* c);
 void reduce_partials(combo_ctx* c, int64_t nblocks, int nred, int slot);
 void fetch_results(combo_ctx* c);  // dres + stats -> hres (sync)
 combo_dev::LawP law_params(const combo_law& L, double* dev_a9);
+void ensure_partials(combo_ctx* c, int64_t count);
+// dfmg.cu
+void dfmg_sweep(combo_ctx* c, const double* fin, const combo_dev::Shift9& sh, double alpha, double* out, int slot);
+void dfmg_tangent_prepare(combo_ctx* c, const double* fin, const combo_dev::Shift9& sh);
+void dfmg_matvec(combo_ctx* c, const double* fin, const combo_dev::Shift9& sh, const double* r, double* pdir,
+                 double beta, bool first, double* q);
 
 // kernel tags for the profiler
 enum ProfTag {

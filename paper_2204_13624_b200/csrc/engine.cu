@@ -171,6 +171,30 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->xW = W;
   p->xT = pick_threads(3 * d[0] * W);
   p->xsmem = size_t(3 * d[0] * W) * sizeof(double2);
+  // register-resident geometry (pow2 axes >= 8): T = lines * N/8
+  if (n3 >= 8) {
+    const int64_t tl = n3 / 8;
+    int64_t Lz = 1;
+    while (((9 * (Lz + 1) + 1) / 2) * tl <= 512 && ((9 * (Lz + 1) + 1) / 2) * n3 * 18 <= 100 * 1024) ++Lz;
+    p->rzL = int(Lz);
+    const int64_t np = (9 * Lz + 1) / 2;
+    p->rzT = int((np * tl + 31) / 32 * 32);
+    p->rzsmem = size_t(np * (n3 + n3 / 8)) * sizeof(double2);
+  }
+  if (d[1] >= 8) {
+    int Wy = int(std::min<int64_t>(8, p->n3c));
+    while (Wy > 1 && Wy * (d[1] / 8) > 512) Wy /= 2;
+    p->ryW = Wy;
+    p->ryT = int(std::max<int64_t>(32, (Wy * (d[1] / 8) + 31) / 32 * 32));
+    p->rysmem = size_t((d[1] + d[1] / 8) * Wy) * sizeof(double2);
+  }
+  if (d[0] >= 8) {
+    int Wx = int(std::min<int64_t>(8, p->n3c));
+    while (Wx > 1 && Wx * (d[0] / 8) > 256) Wx /= 2;
+    p->rxW = Wx;
+    p->rxT = int(std::max<int64_t>(32, (Wx * (d[0] / 8) + 31) / 32 * 32));
+    p->rxsmem = size_t(3 * (d[0] + d[0] / 8) * Wx) * sizeof(double2);
+  }
   p->spec.alloc(size_t(9 * d[0] * d[1] * p->n3p));
   c->plan = std::move(p);
 }
@@ -261,30 +285,55 @@ void dispatch_log2(int64_t n, F&& f) {
 template <class Prod>
 int64_t launch_zfwd(combo_ctx* c, const Prod& prod) {
   FftPlan& p = *c->plan;
-  const int64_t nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
-  if (Prod::NRED) ensure_partials(c, nb * Prod::NRED);
+  int64_t nb = 0;
   ProfScope ps(c, kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS);
   dispatch_log2(p.dims[2], [&](auto Lc) {
-    auto k = zfwd_kernel<Prod, decltype(Lc)::value>;
-    smem_attr(k, p.zsmem);
-    k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, prod, c->partials.p);
+    constexpr int L = decltype(Lc)::value;
+    if constexpr (L >= 3) {
+      nb = (p.dims[0] * p.dims[1] + p.rzL - 1) / p.rzL;
+      auto k = zfwd_rr<Prod, L>;
+      smem_attr(k, p.rzsmem);
+      k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, prod, c->partials.p);
+    } else {
+      nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
+      if (Prod::NRED) ensure_partials(c, nb * Prod::NRED);
+      auto k = zfwd_kernel<Prod, L>;
+      smem_attr(k, p.zsmem);
+      k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, prod, c->partials.p);
+    }
   });
   ++c->launches;
   COMBO_CK(cudaGetLastError());
   return nb;
 }
 
+// partial-sum blocks of the next zinv launch (so the caller can size partials)
+int64_t zinv_blocks(const FftPlan& p) {
+  bool pow2 = false;
+  for (int l = 3; l <= 10; ++l) pow2 = pow2 || p.dims[2] == (int64_t(1) << l);
+  const int64_t L = pow2 ? p.rzL : p.zL;
+  return (p.dims[0] * p.dims[1] + L - 1) / L;
+}
+
 template <class Cons>
 int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
   FftPlan& p = *c->plan;
-  const int64_t nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
+  const int64_t nb = zinv_blocks(p);
   if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
   const double scale = 1.0 / double(c->N);
   ProfScope ps(c, kTagZinv, spec_bytes(c) + 72.0 * double(c->N) * Cons::FIELDS);
   dispatch_log2(p.dims[2], [&](auto Lc) {
-    auto k = zinv_kernel<Cons, decltype(Lc)::value>;
-    smem_attr(k, p.zsmem);
-    k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, scale, cons, c->partials.p);
+    constexpr int L = decltype(Lc)::value;
+    if constexpr (L >= 3) {
+      auto k = zinv_rr<Cons, L>;
+      smem_attr(k, p.rzsmem);
+      k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, c->partials.p);
+    } else {
+      auto k = zinv_kernel<Cons, L>;
+      smem_attr(k, p.zsmem);
+      k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, scale, cons,
+                                                    c->partials.p);
+    }
   });
   ++c->launches;
   COMBO_CK(cudaGetLastError());
@@ -294,12 +343,20 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
 template <bool INV>
 void launch_y(combo_ctx* c, int ncomp = 9) {
   FftPlan& p = *c->plan;
-  dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.dims[0]), unsigned(ncomp));
   ProfScope ps(c, INV ? kTagYinv : kTagYfwd, 2.0 * spec_bytes(c) * ncomp / 9.0);
   dispatch_log2(p.dims[1], [&](auto Lc) {
-    auto k = ypass_kernel<decltype(Lc)::value, INV>;
-    smem_attr(k, p.ysmem);
-    k<<<grid, p.yT, p.ysmem, c->stream>>>(p.sv(), p.ax[1].view(), p.yW);
+    constexpr int L = decltype(Lc)::value;
+    if constexpr (L >= 3) {
+      dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.dims[0]), unsigned(ncomp));
+      auto k = ypass_rr<L, INV>;
+      smem_attr(k, p.rysmem);
+      k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
+    } else {
+      dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.dims[0]), unsigned(ncomp));
+      auto k = ypass_kernel<L, INV>;
+      smem_attr(k, p.ysmem);
+      k<<<grid, p.yT, p.ysmem, c->stream>>>(p.sv(), p.ax[1].view(), p.yW);
+    }
   });
   ++c->launches;
   COMBO_CK(cudaGetLastError());
@@ -308,12 +365,20 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
 void launch_xgamma(combo_ctx* c, int kind) {
   const GreenTables g = green_view(green_plan(c, kind));
   FftPlan& p = *c->plan;
-  dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 3u);
   ProfScope ps(c, kTagXGamma, 2.0 * spec_bytes(c));
   dispatch_log2(p.dims[0], [&](auto Lc) {
-    auto k = xgamma_kernel<decltype(Lc)::value>;
-    smem_attr(k, p.xsmem);
-    k<<<grid, p.xT, p.xsmem, c->stream>>>(p.sv(), p.ax[0].view(), p.xW, g);
+    constexpr int L = decltype(Lc)::value;
+    if constexpr (L >= 3) {
+      dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.dims[1]), 3u);
+      auto k = xgamma_rr<L>;
+      smem_attr(k, p.rxsmem);
+      k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+    } else {
+      dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 3u);
+      auto k = xgamma_kernel<L>;
+      smem_attr(k, p.xsmem);
+      k<<<grid, p.xT, p.xsmem, c->stream>>>(p.sv(), p.ax[0].view(), p.xW, g);
+    }
   });
   ++c->launches;
   COMBO_CK(cudaGetLastError());
@@ -322,13 +387,22 @@ void launch_xgamma(combo_ctx* c, int kind) {
 template <bool INV>
 void launch_x_plain(combo_ctx* c) {
   FftPlan& p = *c->plan;
-  // plain x pass: x tile geometry with a single component per block
-  const size_t smem = size_t(p.dims[0] * p.xW) * sizeof(double2);
-  dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 9u);
   dispatch_log2(p.dims[0], [&](auto Lc) {
-    auto k = xpass_kernel<decltype(Lc)::value, INV>;
-    smem_attr(k, smem);
-    k<<<grid, pick_threads(p.dims[0] * p.xW), smem, c->stream>>>(p.sv(), p.ax[0].view(), p.xW);
+    constexpr int L = decltype(Lc)::value;
+    if constexpr (L >= 3) {
+      const size_t smem = size_t((p.dims[0] + p.dims[0] / 8) * p.rxW) * sizeof(double2);
+      dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.dims[1]), 9u);
+      auto k = xpass_rr<L, INV>;
+      smem_attr(k, smem);
+      k<<<grid, p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW);
+    } else {
+      // plain x pass: x tile geometry with a single component per block
+      const size_t smem = size_t(p.dims[0] * p.xW) * sizeof(double2);
+      dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 9u);
+      auto k = xpass_kernel<L, INV>;
+      smem_attr(k, smem);
+      k<<<grid, pick_threads(p.dims[0] * p.xW), smem, c->stream>>>(p.sv(), p.ax[0].view(), p.xW);
+    }
   });
   ++c->launches;
   COMBO_CK(cudaGetLastError());
@@ -370,6 +444,19 @@ Shift9 zero_shift() {
   Shift9 s;
   for (double& v : s.v) v = 0.0;
   return s;
+}
+
+// packed effective tangents of every composite cell at (F + sh, warm starts)
+void comp_tangents(combo_ctx* c, const double* F, const Shift9& sh) {
+  if (!c->ncomp) return;
+  c->t45.alloc(size_t(45 * c->ncomp));
+  // F gather + meta + warm read, t45 write
+  ProfScope ps(c, kTagOther, double(c->ncomp) * (72.0 + 64.0 + 360.0));
+  const int64_t b = (c->ncomp + 127) / 128;
+  k_comp_tangent<<<unsigned(std::min<int64_t>(b, 148 * 32)), 128, 0, c->stream>>>(c->mp, c->cell_data(), F, sh,
+                                                                                     c->t45.p, c->N);
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
 }
 
 // ------------------------------------------------------- host tensors
@@ -563,6 +650,13 @@ class Solver {
     if (cfg_.max_ls_iterations > 0 && ls_total_ >= cfg_.max_ls_iterations) throw LsBudget{};
     ++ls_total_;
   }
+  // eval_stress (solver.cpp:59-63): per-cell sweep or DFMG
+  void eval_sweep(const double* fin, const Shift9& sh, double alpha, double* out, bool writeback, int slot) {
+    if (cfg_.eval == COMBO_EVAL_DFMG)
+      dfmg_sweep(c_, fin, sh, alpha, out, slot);
+    else
+      sweep(c_, fin, sh, alpha, out, writeback, slot);
+  }
   combo_sweep_stats stats() const {
     const Stats* s = reinterpret_cast<const Stats*>(c_->hres + 64);
     combo_sweep_stats o;
@@ -619,7 +713,7 @@ bool Solver::run_basic(const double* fbar, combo_host::StepRec& rep) {
   if (!(alpha_ > 0.0)) alpha_ = std::max(hi, 1.0);
   for (int it = 1; it <= cfg_.max_outer; ++it) {
     reset_stats(c_);
-    sweep(c_, F_, shF_, alpha_, rb_, true, 0);  // tau = P - alpha F ; P sums -> slot 0
+    eval_sweep(F_, shF_, alpha_, rb_, true, 0);  // tau = P - alpha F ; P sums -> slot 0
     last_eval_ = F_;
     last_eval_shift_ = shF_;
     ConsBasic cons;
@@ -662,13 +756,22 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
   double rr = rr0;
   const double bnorm = std::sqrt(rr);
   if (bnorm == 0.0) return 0;
+  // tangents of this Newton iteration (stress_sweep(&tangents45) /
+  // dfmg_tangent_pass, solver.cpp:72-82)
+  const bool dfmg = cfg_.eval == COMBO_EVAL_DFMG;
+  if (dfmg)
+    dfmg_tangent_prepare(c_, F_, shF_);
+  else
+    comp_tangents(c_, F_, shF_);
   int it = 0;
   double beta = 0.0;
   const int g = ew_grid(N_);
   while (it < cfg_.cg_max) {
-    {
-      // r, pdir (r/w), F, q and cid; composite n, c+-, a
-      ProfScope ps(c_, kTagMatvec, (it == 0 ? 292.0 : 364.0) * double(N_) + 64.0 * double(c_->ncomp));
+    if (dfmg) {
+      dfmg_matvec(c_, F_, shF_, r_, pd_, beta, it == 0, rb_);
+    } else {
+      // r, pdir (r/w), F, q and cid; composite packed tangent
+      ProfScope ps(c_, kTagMatvec, (it == 0 ? 292.0 : 364.0) * double(N_) + 360.0 * double(c_->ncomp));
       k_matvec<<<g, kEwThreads, 0, c_->stream>>>(c_->mp, c_->cell_data(), F_, shF_, r_, pd_, beta,
                                                   it == 0 ? 1 : 0, rb_, N_);
     }
@@ -714,7 +817,7 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
     double ss;
     if (!reuse) {
       reset_stats(c_);
-      sweep(c_, F_, shF_, 0.0, rb_, true, 0);
+      eval_sweep(F_, shF_, 0.0, rb_, true, 0);
       last_eval_ = F_;
       last_eval_shift_ = shF_;
       fetch_results(c_);
@@ -775,7 +878,7 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
       fetch_results(c_);
       for (int q = 0; q < 9; ++q) sh_t.v[q] = fbar[q] - c_->hres[30 + q] / double(N_);
       reset_stats(c_);
-      sweep(c_, Fo_, sh_t, 0.0, rb_, true, 0);
+      eval_sweep(Fo_, sh_t, 0.0, rb_, true, 0);
       last_eval_ = Fo_;
       last_eval_shift_ = sh_t;
       fetch_results(c_);
@@ -838,6 +941,13 @@ void Solver::run(const double* fbar_target, combo_report& report) {
   DBuf<double> backup_f, backup_warm;
   backup_f.alloc(size_t(9 * N_));
   if (c_->ncomp) backup_warm.alloc(size_t(3 * c_->ncomp));
+  DBuf<double> dfmg_backup;  // DfmgState warm starts (solver.cpp:315,330)
+  if (cfg_.eval == COMBO_EVAL_DFMG) {
+    // fresh DfmgState per solve (CellSolver ctor, solver.cpp:55)
+    c_->dfmg_warm.alloc(size_t(3 * 8 * std::max<int64_t>(c_->ncomp, 1)));
+    COMBO_CK(cudaMemsetAsync(c_->dfmg_warm.p, 0, c_->dfmg_warm.n * 8, c_->stream));
+    dfmg_backup.alloc(c_->dfmg_warm.n);
+  }
   try {
     while (t < 1.0 - 1e-12) {
       const double dt_try = std::min(dt, 1.0 - t);
@@ -848,6 +958,9 @@ void Solver::run(const double* fbar_target, combo_report& report) {
       COMBO_CK(cudaMemcpyAsync(backup_f.p, F_, size_t(9 * N_) * sizeof(double), cudaMemcpyDeviceToDevice, c_->stream));
       if (c_->ncomp)
         COMBO_CK(cudaMemcpyAsync(backup_warm.p, c_->warm.p, size_t(3 * c_->ncomp) * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c_->stream));
+      if (dfmg_backup.p)
+        COMBO_CK(cudaMemcpyAsync(dfmg_backup.p, c_->dfmg_warm.p, dfmg_backup.n * sizeof(double),
                                  cudaMemcpyDeviceToDevice, c_->stream));
       pin_mean(fbar);
       combo_host::StepRec rep;
@@ -869,6 +982,9 @@ void Solver::run(const double* fbar_target, combo_report& report) {
       pin_mean(fbar_prev);
       if (c_->ncomp)
         COMBO_CK(cudaMemcpyAsync(c_->warm.p, backup_warm.p, size_t(3 * c_->ncomp) * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, c_->stream));
+      if (dfmg_backup.p)
+        COMBO_CK(cudaMemcpyAsync(c_->dfmg_warm.p, dfmg_backup.p, dfmg_backup.n * sizeof(double),
                                  cudaMemcpyDeviceToDevice, c_->stream));
       ++report.bisections;
       if (report.bisections > cfg_.max_bisections) {
@@ -893,7 +1009,7 @@ void Solver::final_stress(double* P) {
   const double* fin = last_eval_ ? last_eval_ : F_;
   const Shift9 sh = last_eval_ ? last_eval_shift_ : shF_;
   reset_stats(c_);
-  sweep(c_, fin, sh, 0.0, P, false, 40);
+  eval_sweep(fin, sh, 0.0, P, false, 40);
 }
 
 std::string report_json(const combo_report& r) {
@@ -1100,6 +1216,7 @@ int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengt
     if (lam) opts = *lam;
     std::vector<int32_t> cid(static_cast<size_t>(N));
     std::vector<double> nx, ny, nz, cp, cm;
+    std::vector<int64_t> ccell;
     for (int64_t i = 0; i < N; ++i) {
       const size_t si = size_t(i);
       if (hk[si] == 0) {
@@ -1117,6 +1234,7 @@ int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengt
           const double len = std::sqrt(a * a + b * b + d * d);
           if (!(len > 0.0)) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ComboMeta: zero normal");
           cid[si] = int32_t(nx.size());
+          ccell.push_back(i);
           nx.push_back(a / len);
           ny.push_back(b / len);
           nz.push_back(d / len);
@@ -1143,6 +1261,9 @@ int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengt
       COMBO_CK(cudaMemcpy(c->cm.p, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice));
     }
     COMBO_CK(cudaMemset(c->warm.p, 0, 3 * nc * 8));
+    c->ccell.alloc(nc);
+    if (c->ncomp) COMBO_CK(cudaMemcpy(c->ccell.p, ccell.data(), ccell.size() * 8, cudaMemcpyHostToDevice));
+    c->t45.release();
     c->law_m = *matrix;
     c->law_i = *inclusion;
     c->lam = opts;
@@ -1259,6 +1380,7 @@ int combo_tangent_matvec(combo_ctx* c, const double* F, const double* x, double*
     const double* xx = stage_in(c, x, mem, 1);
     double* yy = stage_out(c, y, mem, 2);
     c->scratch[3].alloc(size_t(9 * c->N));
+    comp_tangents(c, f, zero_shift());
     k_matvec<<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), f, zero_shift(), xx,
                                                            c->scratch[3].p, 0.0, 1, yy, c->N);
     ++c->launches;
@@ -1354,8 +1476,6 @@ int combo_solve(combo_ctx* c, const double fbar[9], const combo_solver_cfg* cfg,
     if (cfg->load_steps < 1) throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: load_steps must be >= 1");
     if (!(cfg->tol_equilibrium > 0.0))
       throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: tol_equilibrium must be positive");
-    if (cfg->eval == COMBO_EVAL_DFMG)
-      throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: dfmg evaluation not available in this build");
     if (!(hdet3(fbar) > 0.0)) throw ComboError(COMBO_ERR_INADMISSIBLE_MACRO, "solve: det(fbar) <= 0");
     auto rep = std::make_unique<combo_report>();
     Solver s(c, *cfg);

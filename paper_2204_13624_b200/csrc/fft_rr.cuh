@@ -1,0 +1,389 @@
+// Register-resident Stockham passes for power-of-two line lengths >= 8.
+//
+// Each thread owns one radix-8 butterfly position u of a line (8 complex
+// values in registers; two radix-4 butterflies on radix-4 stages). The first
+// stage reads its operands straight from global memory, intermediate stages
+// exchange through a padded shared-memory tile (conflict-free 128-byte
+// phases), and the last stage leaves the natural-order outputs
+// X[u + r N/8] in registers, from where they are stored to global memory (or,
+// in the X pass, projected by Gamma and fed directly to the inverse transform,
+// whose radix order is reversed so its first stage consumes exactly those
+// registers). Compared with the staged version this halves shared-memory
+// traffic and keeps 8-24 independent 16-byte loads per thread in flight.
+#pragma once
+
+#include "fft.cuh"
+
+namespace combo_dev {
+
+template <int L, bool REV>
+struct Seq {
+  static constexpr int N = 1 << L;
+  static constexpr int NS = pow2_nstages(L);
+  static constexpr int R(int s) { return pow2_radix(L, REV ? NS - 1 - s : s); }
+  static constexpr int P(int s) {
+    int p = 1;
+    for (int i = 0; i < s; ++i) p *= R(i);
+    return p;
+  }
+};
+
+// butterflies of one stage on the 8 register values of a channel
+template <int N, int R, int P, bool INV>
+__device__ __forceinline__ void rr_bfly(double2 (&v)[8], int u, const double2* __restrict__ tw) {
+  constexpr int B = 8 / R;
+  constexpr int TS = N / (P * R);
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    const int t = u + q * (N / 8);
+    const int k = t & (P - 1);
+    if constexpr (P > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        double2 w = __ldg(tw + r * k * TS);
+        if (INV) w.y = -w.y;
+        v[q * R + r] = cmul(v[q * R + r], w);
+      }
+    }
+    dftR<R, INV>(&v[q * R]);
+  }
+}
+
+// output position of register (q, r) after stage (N, R, P)
+template <int N, int R, int P>
+__device__ __forceinline__ int rr_out(int u, int q, int r) {
+  const int t = u + q * (N / 8);
+  const int k = t & (P - 1);
+  return (t - k) * R + k + r * P;
+}
+// input position of register (q, r) for stage (N, R)
+template <int N, int R>
+__device__ __forceinline__ int rr_in(int u, int q, int r) {
+  return u + q * (N / 8) + r * (N / R);
+}
+
+// Stages S.. of the transform on C channels held in v. addr(ch, pos) gives
+// the shared-memory slot of channel ch at line position pos (per thread's
+// line). All threads of the block must call this (barriers inside).
+template <int L, bool INV, bool REV, int S, int C, class Addr>
+__device__ __forceinline__ void rr_stages(double2 (&v)[C][8], int u, bool active, double2* sm,
+                                          const double2* __restrict__ tw, const Addr& addr) {
+  using Q = Seq<L, REV>;
+  if constexpr (S < Q::NS) {
+    constexpr int N = Q::N, R = Q::R(S), P = Q::P(S);
+    if (active) {
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch) rr_bfly<N, R, P, INV>(v[ch], u, tw);
+    }
+    if constexpr (S + 1 < Q::NS) {
+      constexpr int R2 = Q::R(S + 1);
+      if (active) {
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+          for (int q = 0; q < 8 / R; ++q)
+#pragma unroll
+            for (int r = 0; r < R; ++r) sm[addr(ch, rr_out<N, R, P>(u, q, r))] = v[ch][q * R + r];
+      }
+      __syncthreads();
+      if (active) {
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+          for (int q = 0; q < 8 / R2; ++q)
+#pragma unroll
+            for (int r = 0; r < R2; ++r) v[ch][q * R2 + r] = sm[addr(ch, rr_in<N, R2>(u, q, r))];
+      }
+      __syncthreads();
+      rr_stages<L, INV, REV, S + 1, C>(v, u, active, sm, tw, addr);
+    }
+  }
+}
+
+// natural-order output position of register i after the last stage
+template <int L, bool REV>
+__device__ __forceinline__ int rr_final_pos(int u, int i) {
+  using Q = Seq<L, REV>;
+  constexpr int R = Q::R(Q::NS - 1);
+  return rr_in<Q::N, R>(u, i / R, i % R);  // last stage: P = N/R, k = t -> t + r N/R
+}
+// input position of register i for the first stage
+template <int L, bool REV>
+__device__ __forceinline__ int rr_first_pos(int u, int i) {
+  using Q = Seq<L, REV>;
+  constexpr int R = Q::R(0);
+  return rr_in<Q::N, R>(u, i / R, i % R);
+}
+
+// padded element index (one spare slot per 8 elements)
+__device__ __forceinline__ int pad8(int e) { return e + (e >> 3); }
+
+// ---------------------------------------------------------------- reductions
+// Threads are grouped in power-of-two groups of G lanes sharing the same
+// (component a, component b) pair; per group: NSC scalars, plus per-component
+// sums of a and b when PERCOMP. Deterministic fixed-order combination into
+// partials[block][NSC + (PERCOMP ? 9 : 0)].
+template <int NSC, bool PERCOMP>
+__device__ void group_reduce_store(double (&sc)[NSC > 0 ? NSC : 1], double pa, double pb, int ca, int cb, int G,
+                                   double* red_sm, double* partials, int64_t block) {
+  constexpr int NV = NSC + (PERCOMP ? 2 : 0);
+  if constexpr (NV > 0) {
+    double v[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int i = 0; i < NSC; ++i) v[i] = sc[i];
+    if constexpr (PERCOMP) {
+      v[NSC] = pa;
+      v[NSC + 1] = pb;
+    }
+    const int lane = threadIdx.x & 31;
+    const int g = G < 32 ? G : 32;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      for (int o = g >> 1; o > 0; o >>= 1) v[i] += __shfl_down_sync(0xffffffffu, v[i], o, g);
+    const int ngroups = (blockDim.x + g - 1) / g;
+    const int grp = threadIdx.x / g;
+    // red_sm: [ngroups][NV + 2] (values, ca, cb)
+    if ((lane & (g - 1)) == 0) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) red_sm[grp * (NV + 2) + i] = v[i];
+      red_sm[grp * (NV + 2) + NV] = double(ca);
+      red_sm[grp * (NV + 2) + NV + 1] = double(cb);
+    }
+    __syncthreads();
+    constexpr int NOUT = NSC + (PERCOMP ? 9 : 0);
+    if (int(threadIdx.x) < NOUT) {
+      double s = 0.0;
+      const int o = threadIdx.x;
+      for (int gi = 0; gi < ngroups; ++gi) {
+        const double* e = red_sm + gi * (NV + 2);
+        if (o < NSC) {
+          s += e[o];
+        } else if constexpr (PERCOMP) {
+          const int c = o - NSC;
+          if (int(e[NV]) == c) s += e[NSC];
+          if (int(e[NV + 1]) == c) s += e[NSC + 1];
+        }
+      }
+      partials[block * NOUT + o] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ Z pass
+// Pairs of real lines (comp c of z-line l, enumerated rl = 9 l + c) are packed
+// as one complex line; T = npair * N/8 threads, thread -> (pair, u).
+template <class Prod, int L>
+static __global__ void __launch_bounds__(512, 2)
+    zfwd_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, Prod prod, double* partials) {
+  constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
+  extern __shared__ double2 sm[];
+  const int64_t nlines_tot = sv.n1 * sv.n2;
+  const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
+  const int nlines = int(min(int64_t(nl_per_block), nlines_tot - line0));
+  const int nreal = 9 * nlines;
+  const int npair = (nreal + 1) >> 1;
+  const int u = threadIdx.x % TL, p = threadIdx.x / TL;
+  const bool active = p < npair;
+  const int rla = 2 * p, rlb = 2 * p + 1;
+  const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
+  const bool hasb = rlb < nreal;
+  double2 v[1][8];
+  if (active) {
+    const int64_t cella = (line0 + la) * N, cellb = (line0 + lb) * N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = rr_first_pos<L, false>(u, i);
+      v[0][i].x = prod.comp(ca, cella + e);
+      v[0][i].y = hasb ? prod.comp(cb, cellb + e) : 0.0;
+    }
+  }
+  auto addr = [&](int, int pos) { return p * LS + pad8(pos); };
+  rr_stages<L, false, false, 0, 1>(v, u, active, sm, tw, addr);
+  // natural order to smem, then split the pair into two half spectra
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sm[p * LS + pad8(rr_final_pos<L, false>(u, i))] = v[0][i];
+  }
+  __syncthreads();
+  const int nc = int(sv.n3c);
+  for (int t = threadIdx.x; t < npair * nc; t += blockDim.x) {
+    const int pp = t / nc, k = t - pp * nc;
+    const double2 zk = sm[pp * LS + pad8(k)];
+    const double2 zm = sm[pp * LS + pad8(k == 0 ? 0 : N - k)];
+    int rl = 2 * pp;
+    int li = rl / 9, c = rl - 9 * li;
+    sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k] =
+        make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    ++rl;
+    if (rl < nreal) {
+      li = rl / 9;
+      c = rl - 9 * li;
+      sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k] =
+          make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    }
+  }
+}
+
+template <class Cons, int L>
+static __global__ void __launch_bounds__(512, 2)
+    zinv_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, double scale, Cons cons,
+            double* partials) {
+  constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
+  extern __shared__ double2 sm[];
+  const int64_t nlines_tot = sv.n1 * sv.n2;
+  const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
+  const int nlines = int(min(int64_t(nl_per_block), nlines_tot - line0));
+  const int nreal = 9 * nlines;
+  const int npair = (nreal + 1) >> 1;
+  const int nc = int(sv.n3c);
+  // Hermitian completion of the pair (halfcomplex c2r: DC/Nyquist imaginary
+  // parts ignored) into natural-order smem lines
+  for (int t = threadIdx.x; t < npair * nc; t += blockDim.x) {
+    const int pp = t / nc, k = t - pp * nc;
+    int rl = 2 * pp;
+    int li = rl / 9, c = rl - 9 * li;
+    double2 xa = sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k];
+    double2 xb = make_double2(0.0, 0.0);
+    ++rl;
+    if (rl < nreal) {
+      li = rl / 9;
+      c = rl - 9 * li;
+      xb = sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k];
+    }
+    const bool selfconj = (k == 0) || (2 * k == N);
+    if (selfconj) {
+      xa.y = 0.0;
+      xb.y = 0.0;
+    }
+    sm[pp * LS + pad8(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+    if (!selfconj) sm[pp * LS + pad8(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+  }
+  __syncthreads();
+  const int u = threadIdx.x % TL, p = threadIdx.x / TL;
+  const bool active = p < npair;
+  double2 v[1][8];
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[0][i] = sm[p * LS + pad8(rr_first_pos<L, false>(u, i))];
+  }
+  __syncthreads();
+  auto addr = [&](int, int pos) { return p * LS + pad8(pos); };
+  rr_stages<L, true, false, 0, 1>(v, u, active, sm, tw, addr);
+  const int rla = 2 * p, rlb = 2 * p + 1;
+  const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
+  const bool hasb = rlb < nreal;
+  double sc[Cons::NSC > 0 ? Cons::NSC : 1];
+#pragma unroll
+  for (int i = 0; i < (Cons::NSC > 0 ? Cons::NSC : 1); ++i) sc[i] = 0.0;
+  double pa = 0.0, pb = 0.0;
+  if (active) {
+    const int64_t cella = (line0 + la) * N, cellb = (line0 + lb) * N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = rr_final_pos<L, false>(u, i);
+      pa += cons.comp(ca, cella + e, v[0][i].x * scale, sc);
+      if (hasb) pb += cons.comp(cb, cellb + e, v[0][i].y * scale, sc);
+    }
+  }
+  if constexpr (Cons::NSC > 0 || Cons::PERCOMP) {
+    __syncthreads();  // sm reused for the group reduction
+    group_reduce_store<Cons::NSC, Cons::PERCOMP>(sc, pa, pb, ca, active && hasb ? cb : -1, TL,
+                                                 reinterpret_cast<double*>(sm), partials, blockIdx.x);
+  }
+}
+
+// ------------------------------------------------------------------ Y pass
+// W columns (lines) per block, thread -> (line = tid % W, u = tid / W)
+template <int L, bool INV>
+static __global__ void __launch_bounds__(512, 2) ypass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
+  constexpr int N = 1 << L;
+  extern __shared__ double2 sm[];
+  const int c = blockIdx.z, i = blockIdx.y, kc0 = blockIdx.x * W;
+  const int w = min(W, int(sv.n3c) - kc0);
+  const int line = threadIdx.x % W, u = threadIdx.x / W;
+  const bool active = line < w && u < N / 8;
+  double2* base = sv.spec + ((int64_t(c) * sv.n1 + i) * sv.n2) * sv.n3p + kc0 + line;
+  double2 v[1][8];
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[0][q] = base[int64_t(rr_first_pos<L, false>(u, q)) * sv.n3p];
+  }
+  auto addr = [&](int, int pos) { return pad8(pos) * W + line; };
+  rr_stages<L, INV, false, 0, 1>(v, u, active, sm, tw, addr);
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) base[int64_t(rr_final_pos<L, false>(u, q)) * sv.n3p] = v[0][q];
+  }
+}
+
+// ---------------------------------------------------------------- X + Gamma
+// W columns per block, 3 components (row group) per thread.
+template <int L>
+static __global__ void __launch_bounds__(256, 2)
+    xgamma_rr(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G) {
+  constexpr int N = 1 << L;
+  extern __shared__ double2 sm[];
+  const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
+  const int w = min(W, int(sv.n3c) - kc0);
+  const int line = threadIdx.x % W, u = threadIdx.x / W;
+  const bool active = line < w && u < N / 8;
+  const int64_t plane = sv.n1 * sv.n2 * sv.n3p;
+  const int64_t rowstride = sv.n2 * sv.n3p;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.n3p + kc0 + line;
+  double2 v[3][8];
+  if (active) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[ch][q] = base[int64_t(ch) * plane + rr_first_pos<L, false>(u, q) * rowstride];
+  }
+  const int chs = (N + N / 8) * W;  // channel stride in smem
+  auto addr = [&](int ch, int pos) { return ch * chs + pad8(pos) * W + line; };
+  rr_stages<L, false, false, 0, 3>(v, u, active, sm, tw, addr);
+  if (active) {
+    const int64_t k3 = kc0 + line;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t k1 = rr_final_pos<L, false>(u, q);
+      double2 t[3] = {v[0][q], v[1][q], v[2][q]};
+      gamma_row(G, rg, k1, j, k3, sv.n1, sv.n2, sv.n3, t);
+      v[0][q] = t[0];
+      v[1][q] = t[1];
+      v[2][q] = t[2];
+    }
+  }
+  // the reversed radix order's first stage consumes these registers as-is
+  rr_stages<L, true, true, 0, 3>(v, u, active, sm, tw, addr);
+  if (active) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) base[int64_t(ch) * plane + rr_final_pos<L, true>(u, q) * rowstride] = v[ch][q];
+  }
+}
+
+// plain X pass (raw FFT test entry point)
+template <int L, bool INV>
+static __global__ void __launch_bounds__(512, 2) xpass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
+  constexpr int N = 1 << L;
+  extern __shared__ double2 sm[];
+  const int c = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
+  const int w = min(W, int(sv.n3c) - kc0);
+  const int line = threadIdx.x % W, u = threadIdx.x / W;
+  const bool active = line < w && u < N / 8;
+  const int64_t rowstride = sv.n2 * sv.n3p;
+  double2* base = sv.spec + int64_t(c) * sv.n1 * rowstride + int64_t(j) * sv.n3p + kc0 + line;
+  double2 v[1][8];
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[0][q] = base[rr_first_pos<L, false>(u, q) * rowstride];
+  }
+  auto addr = [&](int, int pos) { return pad8(pos) * W + line; };
+  rr_stages<L, INV, false, 0, 1>(v, u, active, sm, tw, addr);
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) base[rr_final_pos<L, false>(u, q) * rowstride] = v[0][q];
+  }
+}
+
+}  // namespace combo_dev

@@ -14,6 +14,7 @@
 #pragma once
 
 #include "fft.cuh"
+#include "fft_rr.cuh"
 #include "material.cuh"
 
 namespace combo_dev {
@@ -28,6 +29,8 @@ struct CellData {
   const double* cm;   // [ncomp]
   double* warm;       // [3][ncomp]
   int64_t ncomp;
+  const int64_t* ccell;  // cell index per composite id
+  const double* t45;     // [45][ncomp] packed composite tangents (or null)
 };
 
 struct Stats {  // device counters (SweepStats)
@@ -136,12 +139,8 @@ static __global__ void __launch_bounds__(kEwThreads) k_matvec(MatParams M, CellD
     }
     const int32_t id = cd.cid[cell];
     if (id >= 0) {
-      const double n[3] = {cd.nrm[id], cd.nrm[cd.ncomp + id], cd.nrm[2 * cd.ncomp + id]};
-      const double a[3] = {cd.warm[id], cd.warm[cd.ncomp + id], cd.warm[2 * cd.ncomp + id]};
-      if (det3(f) > 0.0)
-        laminate_apply(M, f, n, cd.cp[id], cd.cm[id], a, x, y);
-      else
-        for (int c = 0; c < 9; ++c) y[c] = x[c];
+      // composite: packed effective tangent of this Newton iteration
+      packed45_apply(cd.t45 + id, cd.ncomp, x, y);
     } else {
       const LawP L = id == -2 ? M.law[1] : M.law[0];
       NhState s;
@@ -153,6 +152,29 @@ static __global__ void __launch_bounds__(kEwThreads) k_matvec(MatParams M, CellD
     }
 #pragma unroll
     for (int c = 0; c < 9; ++c) q[c * N + cell] = y[c];
+  }
+}
+
+// Packed effective tangents of all composite cells at (F, warm starts): the
+// tangent half of stress_sweep(tangents45) (cell_material.cpp:146-160),
+// evaluated once per Newton iteration.
+static __global__ void __launch_bounds__(128) k_comp_tangent(MatParams M, CellData cd, const double* __restrict__ fin,
+                                                             Shift9 sh, double* __restrict__ t45, int64_t N) {
+  for (int64_t id = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; id < cd.ncomp;
+       id += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t cell = cd.ccell[id];
+    double f[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell] + sh.v[c];
+    const double n[3] = {cd.nrm[id], cd.nrm[cd.ncomp + id], cd.nrm[2 * cd.ncomp + id]};
+    const double a[3] = {cd.warm[id], cd.warm[cd.ncomp + id], cd.warm[2 * cd.ncomp + id]};
+    LamTangent S;
+    if (det3(f) > 0.0) {
+      laminate_prepare(M, f, n, cd.cp[id], cd.cm[id], a, S);
+    } else {
+      S.ok = false;  // inadmissible macro state: identity (cell_material.cpp:134)
+    }
+    laminate_tangent45(M, S, t45 + id, cd.ncomp);
   }
 }
 
@@ -295,6 +317,9 @@ static __global__ void k_reduce_partials(const double* __restrict__ partials, in
 // ------------------------------------------------------------ FFT functors
 // FIELDS = real 9N-field streams (reads + writes) besides the spectrum; used
 // for the algorithmic-bytes bookkeeping of the profiler.
+// Two interfaces: operator() works on all 9 components of a cell (staged
+// generic-size path), comp() on one component (register-resident pow2 path,
+// NSC scalar accumulators + optional per-component sums, see fft_rr.cuh).
 struct ProdLoad9 {
   static constexpr int NRED = 0;
   static constexpr int FIELDS = 1;
@@ -304,16 +329,23 @@ struct ProdLoad9 {
 #pragma unroll
     for (int c = 0; c < 9; ++c) v[c] = src[c * N + cell];
   }
+  __device__ __forceinline__ double comp(int c, int64_t cell) const { return src[c * N + cell]; }
 };
 
 struct ConsStore9 {
   static constexpr int NRED = 0;
+  static constexpr int NSC = 0;
+  static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 1;
   double* dst;
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, const double* v, double*) const {
 #pragma unroll
     for (int c = 0; c < 9; ++c) dst[c * N + cell] = v[c];
+  }
+  __device__ __forceinline__ double comp(int c, int64_t cell, double v, double*) const {
+    dst[c * N + cell] = v;
+    return 0.0;
   }
 };
 
@@ -338,11 +370,22 @@ struct ConsBasic {
       fnew[c * N + cell] = fn;
     }
   }
+  static constexpr int NSC = 1;
+  static constexpr bool PERCOMP = true;
+  __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
+    const double fn = fbar.v[c] - v / alpha;
+    const double d = fn - (fold[c * N + cell] + fold_shift.v[c]);
+    sc[0] += d * d;
+    fnew[c * N + cell] = fn;
+    return fn;
+  }
 };
 
 // Newton residual (solver.cpp:209-225): r = -Pi(P), sum of Pi(P)^2
 struct ConsResid {
   static constexpr int NRED = 1;
+  static constexpr int NSC = 1;
+  static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 1;
   double* r;
   int64_t N;
@@ -353,11 +396,18 @@ struct ConsResid {
       acc[0] += v[c] * v[c];
     }
   }
+  __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
+    r[c * N + cell] = -v;
+    sc[0] += v * v;
+    return 0.0;
+  }
 };
 
 // CG (solver.cpp:180-181): ap = Pi(q), sum of pdir . ap
 struct ConsCg {
   static constexpr int NRED = 1;
+  static constexpr int NSC = 1;
+  static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 2;
   double* ap;
   const double* pdir;
@@ -368,6 +418,11 @@ struct ConsCg {
       ap[c * N + cell] = v[c];
       acc[0] += pdir[c * N + cell] * v[c];
     }
+  }
+  __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
+    ap[c * N + cell] = v;
+    sc[0] += pdir[c * N + cell] * v;
+    return 0.0;
   }
 };
 

@@ -440,51 +440,119 @@ __device__ inline void laminate_solve(const MatParams& M, const double* fbox, co
   R.a[2] = a[2];
 }
 
-// y = A_box x at the stored jump a (matrix-free effective_tangent,
-// laminate.cpp:146-156): y = c+ A+x + c- A-x - dA (z (x) N),
-// z = (D^T (A+/c+ + A-/c-) D)^{-1} D^T dA x.
-__device__ inline void laminate_apply(const MatParams& M, const double* fbox, const double* n,
-                                      double cp, double cm, const double* a, const double* x,
-                                      double* y) {
-  const LawP& Lp = M.law[1];
-  const LawP& Lm = M.law[0];
-  double fp[9], fm[9], pp[9], pm[9];
+// Phase states + factored Newton Hessian of a converged laminate: everything
+// the effective tangent needs (laminate.cpp:146-156).
+struct LamTangent {
   NhState sp, sm;
+  Lu3 lu;
+  double n[3], cp, cm;
+  bool ok;
+};
+
+__device__ inline void laminate_prepare(const MatParams& M, const double* fbox, const double* n, double cp,
+                                        double cm, const double* a, LamTangent& S) {
+  double fp[9], fm[9], pp[9], pm[9];
   form_phases(fbox, n, cp, cm, a, fp, fm);
-  if (!(law_eval(Lp, fp, pp, sp) && law_eval(Lm, fm, pm, sm))) {
+  S.n[0] = n[0];
+  S.n[1] = n[1];
+  S.n[2] = n[2];
+  S.cp = cp;
+  S.cm = cm;
+  S.ok = law_eval(M.law[1], fp, pp, S.sp) && law_eval(M.law[0], fm, pm, S.sm);
+  if (!S.ok) return;
+  double q1[9], q2[9], h[9];
+  law_dtad(M.law[1], S.sp, n, q1);
+  law_dtad(M.law[0], S.sm, n, q2);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) h[i] = q1[i] / cp + q2[i] / cm;
+  S.lu.factor(h);
+}
+
+// y = A_box x (matrix-free effective_tangent): y = c+ A+x + c- A-x
+// - dA (z (x) N), z = (D^T (A+/c+ + A-/c-) D)^{-1} D^T dA x.
+__device__ inline void laminate_apply_prepared(const MatParams& M, const LamTangent& S, const double* x,
+                                               double* y) {
+  if (!S.ok) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) y[i] = x[i];  // identity tangent (cell_material.cpp:134)
     return;
   }
   double u[9], v[9];
-  law_apply(Lp, sp, x, u);
-  law_apply(Lm, sm, x, v);
+  law_apply(M.law[1], S.sp, x, u);
+  law_apply(M.law[0], S.sm, x, v);
   double w[3];
   {
     double d[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) d[i] = u[i] - v[i];
-    mat_n(d, n, w);
+    mat_n(d, S.n, w);
   }
-  double q1[9], q2[9], h[9];
-  law_dtad(Lp, sp, n, q1);
-  law_dtad(Lm, sm, n, q2);
-#pragma unroll
-  for (int i = 0; i < 9; ++i) h[i] = q1[i] / cp + q2[i] / cm;
-  Lu3 lu;
-  lu.factor(h);
   double z[3];
-  lu.solve(w, z);
+  S.lu.solve(w, z);
   double zn[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) zn[3 * i + j] = z[i] * n[j];
+    for (int j = 0; j < 3; ++j) zn[3 * i + j] = z[i] * S.n[j];
   double cu[9], cv[9];
-  law_apply(Lp, sp, zn, cu);
-  law_apply(Lm, sm, zn, cv);
+  law_apply(M.law[1], S.sp, zn, cu);
+  law_apply(M.law[0], S.sm, zn, cv);
 #pragma unroll
-  for (int i = 0; i < 9; ++i) y[i] = (cp * u[i] + cm * v[i]) - (cu[i] - cv[i]);
+  for (int i = 0; i < 9; ++i) y[i] = (S.cp * u[i] + S.cm * v[i]) - (cu[i] - cv[i]);
+}
+
+__device__ inline void laminate_apply(const MatParams& M, const double* fbox, const double* n, double cp,
+                                      double cm, const double* a, const double* x, double* y) {
+  LamTangent S;
+  laminate_prepare(M, fbox, n, cp, cm, a, S);
+  laminate_apply_prepared(M, S, x, y);
+}
+
+// Symmetrized packed upper triangle of A_box (pack45, cell_material.cpp:86-92)
+// from nine matrix-free column applications; t45[t * stride] for t < 45.
+__device__ inline void laminate_tangent45(const MatParams& M, const LamTangent& S, double* t45, int64_t stride) {
+  double v[45];
+#pragma unroll
+  for (int t = 0; t < 45; ++t) v[t] = 0.0;
+#pragma unroll
+  for (int c = 0; c < 9; ++c) {
+    double x[9], y[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) x[i] = i == c ? 1.0 : 0.0;
+    laminate_apply_prepared(M, S, x, y);
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      if (r == c) {
+        v[r * 9 - r * (r - 1) / 2] += y[r];
+      } else if (r < c) {
+        v[r * 9 - r * (r - 1) / 2 + (c - r)] += 0.5 * y[r];
+      } else {
+        v[c * 9 - c * (c - 1) / 2 + (r - c)] += 0.5 * y[r];
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 45; ++t) t45[t * stride] = v[t];
+}
+
+// y = A x with the packed symmetric tangent (tangent_matvec,
+// cell_material.cpp:170-194), t45[t * stride]
+__device__ __forceinline__ void packed45_apply(const double* __restrict__ t45, int64_t stride, const double* x,
+                                               double* y) {
+#pragma unroll
+  for (int c = 0; c < 9; ++c) y[c] = 0.0;
+  int t = 0;
+#pragma unroll
+  for (int r = 0; r < 9; ++r) {
+    const double d = __ldg(t45 + (t++) * stride);
+    y[r] += d * x[r];
+#pragma unroll
+    for (int c = r + 1; c < 9; ++c) {
+      const double a = __ldg(t45 + (t++) * stride);
+      y[r] += a * x[c];
+      y[c] += a * x[r];
+    }
+  }
 }
 
 }  // namespace combo_dev
