@@ -88,8 +88,13 @@ struct FftPlan {
   size_t zsmem = 0, ysmem = 0, xsmem = 0;
   // register-resident pow2 path (fft_rr.cuh), used when the axis length is
   // a power of two >= 8
-  int rzL = 1, rzT = 32, ryW = 8, ryT = 32, rxW = 4, rxT = 32;
+  int rzL = 1, rzT = 32, rzLc = 1, rzTc = 32, ryW = 8, ryT = 32, rxW = 4, rxT = 32;
   size_t rzsmem = 0, rysmem = 0, rxsmem = 0;
+  // persistent double-buffered variants (fft_pp.cuh): buffer sizes (complex)
+  int pzbuf = 0, pybuf = 0, pxbuf = 0;
+  bool pipe_z = false, pipe_y = false, pipe_x = false;
+  int xv = 3;  // X+Gamma kernel variant (2 = xgamma_rr, 3 = xgamma_v3)
+  bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
   DBuf<double2> spec;
   combo_dev::SpecView sv() const {
     combo_dev::SpecView s;
@@ -133,6 +138,7 @@ struct combo_report {
 
 struct combo_ctx {
   int device = 0;
+  int num_sms = 148;
   cudaStream_t stream = nullptr;
   std::string err;
   int64_t launches = 0;
@@ -210,7 +216,7 @@ void dfmg_matvec(combo_ctx* c, const double* fin, const combo_dev::Shift9& sh, c
 // kernel tags for the profiler
 enum ProfTag {
   kTagSweep, kTagMatvec, kTagZfwd, kTagYfwd, kTagXGamma, kTagYinv, kTagZinv, kTagCgUpdate, kTagTrial,
-  kTagMaterialize, kTagReduce, kTagOther, kNumTags
+  kTagMaterialize, kTagReduce, kTagOther, kTagMvZfwd, kNumTags
 };
 // RAII: records CUDA events around the launches in its scope when enabled
 struct ProfScope {

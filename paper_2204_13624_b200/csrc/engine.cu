@@ -7,12 +7,14 @@
 // only scalars (sums, stats) cross PCIe per iteration.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <sstream>
 #include <type_traits>
 
 #include "context.hpp"
+#include "fft_pp.cuh"
 
 using namespace combo_dev;
 
@@ -171,29 +173,55 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->xW = W;
   p->xT = pick_threads(3 * d[0] * W);
   p->xsmem = size_t(3 * d[0] * W) * sizeof(double2);
+  // tuning knobs (benchmarks): COMBO_PIPE_{Z,Y,X}=1 selects the persistent
+  // cp.async pipelines, COMBO_ZLINES / COMBO_YW / COMBO_XW the tile shapes
+  auto knob = [](const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+  };
+  p->pipe_z = knob("COMBO_PIPE_Z", 0) != 0;
+  p->pipe_y = knob("COMBO_PIPE_Y", 0) != 0;
+  p->pipe_x = knob("COMBO_PIPE_X", 0) != 0;
+  p->xv = knob("COMBO_XV", 3);
+  p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;  // fused: 24.7 ms vs 15.5 + 5.7 split (512^3)
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
   if (n3 >= 8) {
     const int64_t tl = n3 / 8;
-    int64_t Lz = 1;
-    while (((9 * (Lz + 1) + 1) / 2) * tl <= 512 && ((9 * (Lz + 1) + 1) / 2) * n3 * 18 <= 100 * 1024) ++Lz;
+    auto lines_for = [&](int64_t tmax) {
+      int64_t Lz = 1;
+      while (((9 * (Lz + 1) + 1) / 2) * tl <= tmax && ((9 * (Lz + 1) + 1) / 2) * n3 * 18 <= 100 * 1024) ++Lz;
+      return Lz;
+    };
+    int64_t Lz = lines_for(512);
+    if (knob("COMBO_ZLINES", 0) > 0) Lz = knob("COMBO_ZLINES", 0);
     p->rzL = int(Lz);
     const int64_t np = (9 * Lz + 1) / 2;
     p->rzT = int((np * tl + 31) / 32 * 32);
+    // fused matvec producer: <= 384 threads (register budget of the NH code)
+    p->rzLc = int(lines_for(384));
+    p->rzTc = int((((9 * p->rzLc + 1) / 2) * tl + 31) / 32 * 32);
     p->rzsmem = size_t(np * (n3 + n3 / 8)) * sizeof(double2);
+    const int64_t ls = n3 + n3 / 8, lsd = (ls + 1) & ~int64_t(1);
+    p->pzbuf = int(std::max({np * ls, (9 * Lz * lsd + 1) / 2, 9 * Lz * p->n3p}));
   }
   if (d[1] >= 8) {
     int Wy = int(std::min<int64_t>(8, p->n3c));
-    while (Wy > 1 && Wy * (d[1] / 8) > 512) Wy /= 2;
+    // 256-thread tiles measured faster than 512 at n2 = 512 (4.5 vs 4.8 ms)
+    while (Wy > 1 && Wy * (d[1] / 8) > 256) Wy /= 2;
+    if (knob("COMBO_YW", 0) > 0) Wy = knob("COMBO_YW", 0);
     p->ryW = Wy;
     p->ryT = int(std::max<int64_t>(32, (Wy * (d[1] / 8) + 31) / 32 * 32));
     p->rysmem = size_t((d[1] + d[1] / 8) * Wy) * sizeof(double2);
+    p->pybuf = int((d[1] + d[1] / 8) * Wy);
   }
   if (d[0] >= 8) {
     int Wx = int(std::min<int64_t>(8, p->n3c));
     while (Wx > 1 && Wx * (d[0] / 8) > 256) Wx /= 2;
+    if (knob("COMBO_XW", 0) > 0) Wx = knob("COMBO_XW", 0);
     p->rxW = Wx;
     p->rxT = int(std::max<int64_t>(32, (Wx * (d[0] / 8) + 31) / 32 * 32));
     p->rxsmem = size_t(3 * (d[0] + d[0] / 8) * Wx) * sizeof(double2);
+    p->pxbuf = int(3 * (d[0] + d[0] / 8) * Wx);
   }
   p->spec.alloc(size_t(9 * d[0] * d[1] * p->n3p));
   c->plan = std::move(p);
@@ -236,7 +264,7 @@ cudaEvent_t pool_event(combo_ctx* c) {
   return e;
 }
 const char* kTagNames[kNumTags] = {"sweep",  "matvec",    "zfwd",      "yfwd",   "xgamma", "yinv",
-                                   "zinv",   "cg_update", "trial",     "materialize", "reduce", "other"};
+                                   "zinv",   "cg_update", "trial",     "materialize", "reduce", "other", "matvec_zfwd"};
 }  // namespace
 
 ProfScope::ProfScope(combo_ctx* ctx, int tag, double bytes) : c(ctx) {
@@ -282,18 +310,49 @@ void dispatch_log2(int64_t n, F&& f) {
   }
 }
 
+// persistent grid: resident blocks per SM x SMs, capped by the tile count
+template <class K>
+int pp_grid(const combo_ctx* c, K kernel, int threads, size_t smem, int64_t ntiles) {
+  int occ = 0;
+  COMBO_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
+  if (occ < 1) throw ComboError(COMBO_ERR_CUDA, "FFT pass does not fit on an SM");
+  return int(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(occ) * c->num_sms)));
+}
+
+bool pp_axis(int64_t n) {
+  for (int l = 3; l <= 10; ++l)
+    if (n == (int64_t(1) << l)) return true;
+  return false;
+}
+
 template <class Prod>
-int64_t launch_zfwd(combo_ctx* c, const Prod& prod) {
+int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
   FftPlan& p = *c->plan;
   int64_t nb = 0;
-  ProfScope ps(c, kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS);
+  ProfScope ps(c, Prod::CELL ? kTagMvZfwd : kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      nb = (p.dims[0] * p.dims[1] + p.rzL - 1) / p.rzL;
-      auto k = zfwd_rr<Prod, L>;
-      smem_attr(k, p.rzsmem);
-      k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, prod, c->partials.p);
+      const int64_t ntiles = (p.dims[0] * p.dims[1] + p.rzL - 1) / p.rzL;
+      bool piped = false;
+      if constexpr (!Prod::CELL) {
+        if (p.pipe_z) {
+          const size_t smem = size_t(2 * p.pzbuf) * sizeof(double2);
+          auto k = zfwd_pp<Prod, L>;
+          smem_attr(k, smem);
+          nb = pp_grid(c, k, p.rzT, smem, ntiles);
+          k<<<unsigned(nb), p.rzT, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, ntiles, p.pzbuf, prod);
+          piped = true;
+        }
+      }
+      if (!piped) {
+        const int lz = Prod::CELL ? p.rzLc : p.rzL;
+        nb = (p.dims[0] * p.dims[1] + lz - 1) / lz;
+        auto k = zfwd_rr<Prod, L>;
+        smem_attr(k, p.rzsmem);
+        k<<<unsigned(nb), Prod::CELL ? p.rzTc : p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, lz, prod,
+                                                                            c->partials.p);
+      }
     } else {
       nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
       if (Prod::NRED) ensure_partials(c, nb * Prod::NRED);
@@ -307,28 +366,34 @@ int64_t launch_zfwd(combo_ctx* c, const Prod& prod) {
   return nb;
 }
 
-// partial-sum blocks of the next zinv launch (so the caller can size partials)
-int64_t zinv_blocks(const FftPlan& p) {
-  bool pow2 = false;
-  for (int l = 3; l <= 10; ++l) pow2 = pow2 || p.dims[2] == (int64_t(1) << l);
-  const int64_t L = pow2 ? p.rzL : p.zL;
-  return (p.dims[0] * p.dims[1] + L - 1) / L;
-}
-
 template <class Cons>
 int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
   FftPlan& p = *c->plan;
-  const int64_t nb = zinv_blocks(p);
-  if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
+  int64_t nb = 0;
   const double scale = 1.0 / double(c->N);
   ProfScope ps(c, kTagZinv, spec_bytes(c) + 72.0 * double(c->N) * Cons::FIELDS);
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      auto k = zinv_rr<Cons, L>;
-      smem_attr(k, p.rzsmem);
-      k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, c->partials.p);
+      const int64_t ntiles = (p.dims[0] * p.dims[1] + p.rzL - 1) / p.rzL;
+      if (p.pipe_z) {
+        const size_t smem = size_t(2 * p.pzbuf) * sizeof(double2);
+        auto k = zinv_pp<Cons, L>;
+        smem_attr(k, smem);
+        nb = pp_grid(c, k, p.rzT, smem, ntiles);
+        if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
+        k<<<unsigned(nb), p.rzT, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, ntiles, p.pzbuf, scale, cons,
+                                                    c->partials.p);
+      } else {
+        nb = ntiles;
+        if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
+        auto k = zinv_rr<Cons, L>;
+        smem_attr(k, p.rzsmem);
+        k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, c->partials.p);
+      }
     } else {
+      nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
+      if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
       auto k = zinv_kernel<Cons, L>;
       smem_attr(k, p.zsmem);
       k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, scale, cons,
@@ -347,10 +412,19 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
   dispatch_log2(p.dims[1], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.dims[0]), unsigned(ncomp));
-      auto k = ypass_rr<L, INV>;
-      smem_attr(k, p.rysmem);
-      k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
+      if (p.pipe_y) {
+        const int64_t ntiles = ((p.n3c + p.ryW - 1) / p.ryW) * p.dims[0] * ncomp;
+        const size_t smem = size_t(2 * p.pybuf) * sizeof(double2);
+        auto k = ypass_pp<L, INV>;
+        smem_attr(k, smem);
+        const int g = pp_grid(c, k, p.ryT, smem, ntiles);
+        k<<<unsigned(g), p.ryT, smem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW, ntiles, p.pybuf);
+      } else {
+        dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.dims[0]), unsigned(ncomp));
+        auto k = ypass_rr<L, INV>;
+        smem_attr(k, p.rysmem);
+        k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
+      }
     } else {
       dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.dims[0]), unsigned(ncomp));
       auto k = ypass_kernel<L, INV>;
@@ -369,10 +443,29 @@ void launch_xgamma(combo_ctx* c, int kind) {
   dispatch_log2(p.dims[0], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.dims[1]), 3u);
-      auto k = xgamma_rr<L>;
-      smem_attr(k, p.rxsmem);
-      k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+      if (p.pipe_x) {
+        const int64_t ntiles = ((p.n3c + p.rxW - 1) / p.rxW) * p.dims[1] * 3;
+        const size_t smem = size_t(2 * p.pxbuf) * sizeof(double2);
+        auto k = xgamma_pp<L>;
+        smem_attr(k, smem);
+        const int gr = pp_grid(c, k, p.rxT, smem, ntiles);
+        k<<<unsigned(gr), p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g, ntiles, p.pxbuf);
+      } else {
+        dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.dims[1]), 3u);
+        if (p.xv == 3 && p.rxT <= 256) {
+          auto k = xgamma_v3<L, 256, 2>;
+          smem_attr(k, p.rxsmem);
+          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+        } else if (p.xv >= 3) {
+          auto k = xgamma_v3<L, 512, 1>;
+          smem_attr(k, p.rxsmem);
+          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+        } else {
+          auto k = xgamma_rr<L>;
+          smem_attr(k, p.rxsmem);
+          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+        }
+      }
     } else {
       dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 3u);
       auto k = xgamma_kernel<L>;
@@ -383,7 +476,6 @@ void launch_xgamma(combo_ctx* c, int kind) {
   ++c->launches;
   COMBO_CK(cudaGetLastError());
 }
-
 template <bool INV>
 void launch_x_plain(combo_ctx* c) {
   FftPlan& p = *c->plan;
@@ -410,8 +502,9 @@ void launch_x_plain(combo_ctx* c) {
 // Projection Pi(tau) = alpha Gamma^0 tau (green.cpp:133-151) with fused
 // producer / consumer. Returns the partial-block counts via nbp / nbc.
 template <class Prod, class Cons>
-void project_fused(combo_ctx* c, int kind, const Prod& prod, const Cons& cons, int slot_prod, int slot_cons) {
-  const int64_t nbp = launch_zfwd(c, prod);
+void project_fused(combo_ctx* c, int kind, const Prod& prod, const Cons& cons, int slot_prod, int slot_cons,
+                   double prod_bytes = 0.0) {
+  const int64_t nbp = launch_zfwd(c, prod, prod_bytes);
   if (Prod::NRED) reduce_partials(c, nbp, Prod::NRED, slot_prod);
   launch_y<false>(c);
   launch_xgamma(c, kind);
@@ -764,46 +857,75 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
   else
     comp_tangents(c_, F_, shF_);
   int it = 0;
-  double beta = 0.0;
+  double beta = 0.0, step_prev = 0.0;
   const int g = ew_grid(N_);
-  while (it < cfg_.cg_max) {
-    if (dfmg) {
-      dfmg_matvec(c_, F_, shF_, r_, pd_, beta, it == 0, rb_);
-    } else {
-      // r, pdir (r/w), F, q and cid; composite packed tangent
-      ProfScope ps(c_, kTagMatvec, (it == 0 ? 292.0 : 364.0) * double(N_) + 360.0 * double(c_->ncomp));
-      k_matvec<<<g, kEwThreads, 0, c_->stream>>>(c_->mp, c_->cell_data(), F_, shF_, r_, pd_, beta,
-                                                  it == 0 ? 1 : 0, rb_, N_);
-    }
+  // x += step * pdir is deferred into the next matvec (which reads pdir
+  // anyway); the last pending update is flushed on exit (solver.cpp:186)
+  auto flush_x = [&]() {
+    if (dfmg || it == 0) return;
+    ProfScope ps(c_, kTagCgUpdate, 216.0 * double(N_));
+    k_axpy<<<ew_grid(9 * N_), kEwThreads, 0, c_->stream>>>(x_, pd_, step_prev, 9 * N_);
     ++c_->launches;
     COMBO_CK(cudaGetLastError());
-    ProdLoad9 prod{rb_, N_};
+  };
+  while (it < cfg_.cg_max) {
     ConsCg cons{ap_, pd_, N_};
     count_ls();
     ++rep.ls_cg;
-    project_fused(c_, cfg_.green, prod, cons, 0, 20);
+    if (dfmg) {
+      dfmg_matvec(c_, F_, shF_, r_, pd_, beta, it == 0, rb_);
+      ++c_->launches;
+      COMBO_CK(cudaGetLastError());
+      project_fused(c_, cfg_.green, ProdLoad9{rb_, N_}, cons, 0, 20);
+    } else {
+      // matvec fused into the Z-forward pass: r, F, cid, pdir (r/w), x (r/w,
+      // deferred update); composite packed tangents
+      ProdMatvec prod{{c_->mp, c_->cell_data(), F_, shF_, r_, pd_, beta, it == 0 ? 1 : 0, N_, x_, step_prev}};
+      const double mvb = (it == 0 ? 220.0 : 436.0) * double(N_) + 360.0 * double(c_->ncomp);
+      if (c_->plan->fuse_mv) {
+        project_fused(c_, cfg_.green, prod, cons, 0, 20, mvb);
+      } else {
+        {
+          ProfScope ps(c_, kTagMatvec, mvb + 72.0 * double(N_));
+          k_matvec<<<g, kEwThreads, 0, c_->stream>>>(prod.a, rb_);
+        }
+        ++c_->launches;
+        COMBO_CK(cudaGetLastError());
+        project_fused(c_, cfg_.green, ProdLoad9{rb_, N_}, cons, 0, 20);
+      }
+    }
     fetch_results(c_);
     const double pap = c_->hres[20];
     if (!(pap > 0.0)) {
       breakdown = true;
-      return it;
+      return it;  // this iteration's x update is not applied (solver.cpp:182-185)
     }
     const double step = rr / pap;
+    if (dfmg) {
+      ProfScope ps(c_, kTagCgUpdate, 216.0 * double(N_));
+      k_axpy<<<ew_grid(9 * N_), kEwThreads, 0, c_->stream>>>(x_, pd_, step, 9 * N_);
+      ++c_->launches;
+    }
     ensure_partials(c_, g);
     {
-      ProfScope ps(c_, kTagCgUpdate, 432.0 * double(N_));
-      k_cg_update<<<g, kEwThreads, 0, c_->stream>>>(x_, r_, pd_, ap_, step, 9 * N_, c_->partials.p);
+      ProfScope ps(c_, kTagCgUpdate, 216.0 * double(N_));
+      k_cg_update<<<g, kEwThreads, 0, c_->stream>>>(r_, ap_, step, 9 * N_, c_->partials.p);
     }
     ++c_->launches;
     COMBO_CK(cudaGetLastError());
     reduce_partials(c_, g, 1, 21);
     fetch_results(c_);
     ++it;
+    step_prev = step;
     const double rr_new = c_->hres[21];
-    if (std::sqrt(rr_new) <= tol_rel * bnorm) return it;
+    if (std::sqrt(rr_new) <= tol_rel * bnorm) {
+      flush_x();
+      return it;
+    }
     beta = rr_new / rr;
     rr = rr_new;
   }
+  flush_x();
   return it;
 }
 
@@ -1109,6 +1231,7 @@ int combo_ctx_create(int device, combo_ctx** out) {
     COMBO_CK(cudaGetDeviceCount(&n));
     if (device < 0 || device >= n) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "no such CUDA device");
     COMBO_CK(cudaSetDevice(device));
+    COMBO_CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     COMBO_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     ensure_scratch(c);
   });
@@ -1381,8 +1504,8 @@ int combo_tangent_matvec(combo_ctx* c, const double* F, const double* x, double*
     double* yy = stage_out(c, y, mem, 2);
     c->scratch[3].alloc(size_t(9 * c->N));
     comp_tangents(c, f, zero_shift());
-    k_matvec<<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), f, zero_shift(), xx,
-                                                           c->scratch[3].p, 0.0, 1, yy, c->N);
+    MatvecArgs a{c->mp, c->cell_data(), f, zero_shift(), xx, c->scratch[3].p, 0.0, 1, c->N, nullptr, 0.0};
+    k_matvec<<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(a, yy);
     ++c->launches;
     COMBO_CK(cudaGetLastError());
     finish_out(c, y, yy, mem, size_t(9 * c->N));

@@ -173,7 +173,7 @@ __device__ void group_reduce_store(double (&sc)[NSC > 0 ? NSC : 1], double pa, d
 // Pairs of real lines (comp c of z-line l, enumerated rl = 9 l + c) are packed
 // as one complex line; T = npair * N/8 threads, thread -> (pair, u).
 template <class Prod, int L>
-static __global__ void __launch_bounds__(512, 2)
+static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
     zfwd_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, Prod prod, double* partials) {
   constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
   extern __shared__ double2 sm[];
@@ -188,7 +188,29 @@ static __global__ void __launch_bounds__(512, 2)
   const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
   const bool hasb = rlb < nreal;
   double2 v[1][8];
-  if (active) {
+  if constexpr (Prod::CELL) {
+    // per-cell producer: all 9 components of the block's cells into the
+    // pair lines in shared memory, then the first stage reads from there
+    double* smd = reinterpret_cast<double*>(sm);
+    for (int t = threadIdx.x; t < nlines * N; t += blockDim.x) {
+      const int l = t >> L, k = t & (N - 1);
+      double y[9];
+      prod(line0 * N + t, y, nullptr);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        const int rl = 9 * l + c;
+        smd[2 * ((rl >> 1) * LS + pad8(k)) + (rl & 1)] = y[c];
+      }
+    }
+    if (nreal & 1)
+      for (int k = threadIdx.x; k < N; k += blockDim.x) smd[2 * ((npair - 1) * LS + pad8(k)) + 1] = 0.0;
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[0][i] = sm[p * LS + pad8(rr_first_pos<L, false>(u, i))];
+    }
+    __syncthreads();
+  } else if (active) {
     const int64_t cella = (line0 + la) * N, cellb = (line0 + lb) * N;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -353,6 +375,140 @@ static __global__ void __launch_bounds__(256, 2)
     }
   }
   // the reversed radix order's first stage consumes these registers as-is
+  rr_stages<L, true, true, 0, 3>(v, u, active, sm, tw, addr);
+  if (active) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) base[int64_t(ch) * plane + rr_final_pos<L, true>(u, q) * rowstride] = v[ch][q];
+  }
+}
+
+// Gamma with the per-column factors hoisted out of the k1 loop: a thread's
+// column (k2, k3) is fixed, so the rotated symbol g = (f1 a2 a3, f2 a1 a3,
+// f3 a1 a2) costs three complex products per k-point, and the 1/den scaling
+// one reciprocal (green.cpp:67-130 up to the rounding of the factor order).
+struct GammaCol {
+  double2 c0, c1, c2;  // per-column factors of g0, g1, g2
+  double d12;          // continuous: xi1^2 + xi2^2
+  bool nyq;            // continuous: an axis of the column is at Nyquist
+};
+
+__device__ __forceinline__ GammaCol gamma_col(const GreenTables& G, int64_t k2, int64_t k3, int64_t n2,
+                                              int64_t n3) {
+  GammaCol c;
+  if (G.kind == 0) {
+    c.c1 = make_double2(0.0, G.xi[1][k2]);
+    c.c2 = make_double2(0.0, G.xi[2][k3]);
+    c.d12 = c.c1.y * c.c1.y + c.c2.y * c.c2.y;
+    c.nyq = 2 * k2 == n2 || 2 * k3 == n3;
+    c.c0 = make_double2(0.0, 0.0);
+  } else if (G.kind == 1) {
+    const double2 a2 = G.avg[1][k2], a3 = G.avg[2][k3];
+    c.c0 = cmul(a2, a3);
+    c.c1 = cmul(G.fwd[1][k2], a3);
+    c.c2 = cmul(G.fwd[2][k3], a2);
+    c.d12 = 0.0;
+    c.nyq = false;
+  } else {
+    c.c1 = G.fwd[1][k2];
+    c.c2 = G.fwd[2][k3];
+    c.c0 = make_double2(0.0, 0.0);
+    c.d12 = 0.0;
+    c.nyq = false;
+  }
+  return c;
+}
+
+__device__ __forceinline__ void gamma_row_col(const GreenTables& G, const GammaCol& c, int row, int64_t k1,
+                                              int64_t n1, double2* t) {
+  if (G.kind == 0) {
+    if (c.nyq || 2 * k1 == n1) {
+      t[0] = t[1] = t[2] = make_double2(0.0, 0.0);
+      return;
+    }
+    const double x0 = G.xi[0][k1];
+    const double den = x0 * x0 + c.d12;
+    if (den == 0.0) {
+      t[0] = t[1] = t[2] = make_double2(0.0, 0.0);
+      return;
+    }
+    // g = i xi: tau_J = xi_J (sum_L xi_L tau_L) / den
+    const double sx = x0 * t[0].x + c.c1.y * t[1].x + c.c2.y * t[2].x;
+    const double sy = x0 * t[0].y + c.c1.y * t[1].y + c.c2.y * t[2].y;
+    const double r = 1.0 / den;
+    const double x[3] = {x0 * r, c.c1.y * r, c.c2.y * r};
+#pragma unroll
+    for (int J = 0; J < 3; ++J) t[J] = make_double2(x[J] * sx, x[J] * sy);
+    return;
+  }
+  double2 g[3];
+  if (G.kind == 1) {
+    const double2 a1 = G.avg[0][k1];
+    g[0] = cmul(G.fwd[0][k1], c.c0);
+    g[1] = cmul(c.c1, a1);
+    g[2] = cmul(c.c2, a1);
+  } else {
+    g[0] = G.fwd[0][k1];
+    g[1] = c.c1;
+    g[2] = c.c2;
+  }
+  const double den = (g[0].x * g[0].x + g[0].y * g[0].y) + (g[1].x * g[1].x + g[1].y * g[1].y) +
+                     (g[2].x * g[2].x + g[2].y * g[2].y);
+  if (den == 0.0) {
+    t[0] = t[1] = t[2] = make_double2(0.0, 0.0);
+    return;
+  }
+  double2 gr[3];
+#pragma unroll
+  for (int J = 0; J < 3; ++J) gr[J] = (G.kind == 2 && J != row) ? make_double2(-g[J].x, g[J].y) : g[J];
+  double sx = 0.0, sy = 0.0;
+#pragma unroll
+  for (int L = 0; L < 3; ++L) {
+    sx += gr[L].x * t[L].x + gr[L].y * t[L].y;
+    sy += gr[L].x * t[L].y - gr[L].y * t[L].x;
+  }
+  const double r = 1.0 / den;
+  const double2 s = make_double2(sx * r, sy * r);
+#pragma unroll
+  for (int J = 0; J < 3; ++J) t[J] = cmul(gr[J], s);
+}
+
+// X + Gamma, variant 3: column-hoisted Gamma; MAXT = launch bound (256 with
+// 2 blocks/SM, or 512 with W = 8 and 1 block/SM).
+template <int L, int MAXT, int MINB>
+static __global__ void __launch_bounds__(MAXT, MINB)
+    xgamma_v3(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G) {
+  constexpr int N = 1 << L;
+  extern __shared__ double2 sm[];
+  const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
+  const int w = min(W, int(sv.n3c) - kc0);
+  const int line = threadIdx.x % W, u = threadIdx.x / W;
+  const bool active = line < w && u < N / 8;
+  const int64_t plane = sv.n1 * sv.n2 * sv.n3p;
+  const int64_t rowstride = sv.n2 * sv.n3p;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.n3p + kc0 + line;
+  double2 v[3][8];
+  if (active) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[ch][q] = base[int64_t(ch) * plane + rr_first_pos<L, false>(u, q) * rowstride];
+  }
+  const int chs = (N + N / 8) * W;
+  auto addr = [&](int ch, int pos) { return ch * chs + pad8(pos) * W + line; };
+  rr_stages<L, false, false, 0, 3>(v, u, active, sm, tw, addr);
+  if (active) {
+    const GammaCol col = gamma_col(G, j, kc0 + line, sv.n2, sv.n3);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      double2 t[3] = {v[0][q], v[1][q], v[2][q]};
+      gamma_row_col(G, col, rg, rr_final_pos<L, false>(u, q), sv.n1, t);
+      v[0][q] = t[0];
+      v[1][q] = t[1];
+      v[2][q] = t[2];
+    }
+  }
   rr_stages<L, true, true, 0, 3>(v, u, active, sm, tw, addr);
   if (active) {
 #pragma unroll

@@ -119,39 +119,72 @@ static __global__ void __launch_bounds__(kEwThreads) k_sweep(MatParams M, CellDa
   block_reduce_store<9>(acc, partials, blockIdx.x);
 }
 
-// pdir = first ? r : r + beta * pdir ; q = A(F) : pdir   (matrix free)
-static __global__ void __launch_bounds__(kEwThreads) k_matvec(MatParams M, CellData cd, const double* __restrict__ fin,
-                                                       Shift9 sh, const double* __restrict__ r, double* pdir,
-                                                       double beta, int first, double* __restrict__ q,
-                                                       int64_t N) {
-  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
+// CG step P1 (solver.cpp:186-197, deferred): x += step_prev * pdir_old (the
+// x update of the previous iteration, applied where pdir_old is read anyway),
+// pdir = first ? r : r + beta * pdir_old ; y = A(F) : pdir (matrix free NH,
+// packed tangent for composites) for one cell. x may be null (operator-level
+// calls).
+struct MatvecArgs {
+  MatParams M;
+  CellData cd;
+  const double* fin;
+  Shift9 sh;
+  const double* r;
+  double* pdir;
+  double beta;
+  int first;
+  int64_t N;
+  double* xv;
+  double step_prev;
+};
+
+__device__ __forceinline__ void mv_cell(const MatvecArgs& a, int64_t cell, double* y) {
+  const int64_t N = a.N;
+  // all loads are issued before any store (pdir / xv may not be reordered
+  // across stores by the compiler otherwise)
+  double f[9], x[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) x[c] = __ldg(a.r + c * N + cell);
+#pragma unroll
+  for (int c = 0; c < 9; ++c) f[c] = __ldg(a.fin + c * N + cell) + a.sh.v[c];
+  if (!a.first) {
+    double po[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) po[c] = a.pdir[c * N + cell];
+    if (a.xv) {
+      double xo[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) xo[c] = a.xv[c * N + cell];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) a.xv[c * N + cell] = xo[c] + a.step_prev * po[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) x[c] += a.beta * po[c];
+  }
+#pragma unroll
+  for (int c = 0; c < 9; ++c) a.pdir[c * N + cell] = x[c];
+  const int32_t id = a.cd.cid[cell];
+  if (id >= 0) {
+    // composite: packed effective tangent of this Newton iteration
+    packed45_apply(a.cd.t45 + id, a.cd.ncomp, x, y);
+  } else {
+    const LawP L = id == -2 ? a.M.law[1] : a.M.law[0];
+    NhState s;
+    double p[9];
+    if (law_eval(L, f, p, s))
+      law_apply(L, s, x, y);
+    else
+      for (int c = 0; c < 9; ++c) y[c] = x[c];
+  }
+}
+
+static __global__ void __launch_bounds__(kEwThreads) k_matvec(MatvecArgs a, double* __restrict__ q) {
+  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < a.N;
        cell += int64_t(gridDim.x) * blockDim.x) {
-    double f[9], x[9], y[9];
+    double y[9];
+    mv_cell(a, cell, y);
 #pragma unroll
-    for (int c = 0; c < 9; ++c) {
-      const double rv = r[c * N + cell];
-      x[c] = first ? rv : rv + beta * pdir[c * N + cell];
-      f[c] = fin[c * N + cell] + sh.v[c];
-    }
-    if (!first || pdir != r) {
-#pragma unroll
-      for (int c = 0; c < 9; ++c) pdir[c * N + cell] = x[c];
-    }
-    const int32_t id = cd.cid[cell];
-    if (id >= 0) {
-      // composite: packed effective tangent of this Newton iteration
-      packed45_apply(cd.t45 + id, cd.ncomp, x, y);
-    } else {
-      const LawP L = id == -2 ? M.law[1] : M.law[0];
-      NhState s;
-      double p[9];
-      if (law_eval(L, f, p, s))
-        law_apply(L, s, x, y);
-      else
-        for (int c = 0; c < 9; ++c) y[c] = x[c];
-    }
-#pragma unroll
-    for (int c = 0; c < 9; ++c) q[c * N + cell] = y[c];
+    for (int c = 0; c < 9; ++c) q[c * a.N + cell] = y[c];
   }
 }
 
@@ -178,19 +211,23 @@ static __global__ void __launch_bounds__(128) k_comp_tangent(MatParams M, CellDa
   }
 }
 
-// Flat 9N update: x += step * p ; r -= step * ap ; partial sum of r^2
-static __global__ void __launch_bounds__(kEwThreads) k_cg_update(double* __restrict__ x, double* __restrict__ r,
-                                                          const double* __restrict__ p,
+// CG step P6 (solver.cpp:187-190): r -= step * ap ; partial sum of r^2
+static __global__ void __launch_bounds__(kEwThreads) k_cg_update(double* __restrict__ r,
                                                           const double* __restrict__ ap, double step,
                                                           int64_t n, double* partials) {
   double acc[1] = {0.0};
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    x[i] += step * p[i];
     const double rv = r[i] + (-step) * ap[i];
     r[i] = rv;
     acc[0] += rv * rv;
   }
   block_reduce_store<1>(acc, partials, blockIdx.x);
+}
+
+// pending x += step * pdir of the last CG iteration (solver.cpp:186)
+static __global__ void k_axpy(double* __restrict__ x, const double* __restrict__ p, double step, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    x[i] += step * p[i];
 }
 
 // ftrial = (F + shiftF) + s x ; per-component sums for pin_mean
@@ -323,6 +360,7 @@ static __global__ void k_reduce_partials(const double* __restrict__ partials, in
 struct ProdLoad9 {
   static constexpr int NRED = 0;
   static constexpr int FIELDS = 1;
+  static constexpr bool CELL = false;  // comp() interface
   const double* src;
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, double* v, double*) const {
@@ -330,6 +368,18 @@ struct ProdLoad9 {
     for (int c = 0; c < 9; ++c) v[c] = src[c * N + cell];
   }
   __device__ __forceinline__ double comp(int c, int64_t cell) const { return src[c * N + cell]; }
+};
+
+// CG matvec fused into the Z-forward pass (solver.cpp:194-197): the block
+// evaluates y = A : pdir for the cells of its z-lines into shared memory and
+// transforms them directly, so q never touches HBM. CELL producers use the
+// per-cell operator() on every path.
+struct ProdMatvec {
+  static constexpr int NRED = 0;
+  static constexpr int FIELDS = 0;  // bytes passed by the caller (first / later iterations differ)
+  static constexpr bool CELL = true;
+  MatvecArgs a;
+  __device__ __forceinline__ void operator()(int64_t cell, double* v, double*) const { mv_cell(a, cell, v); }
 };
 
 struct ConsStore9 {
