@@ -182,7 +182,7 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->pipe_z = knob("COMBO_PIPE_Z", 0) != 0;
   p->pipe_y = knob("COMBO_PIPE_Y", 0) != 0;
   p->pipe_x = knob("COMBO_PIPE_X", 0) != 0;
-  p->xv = knob("COMBO_XV", 3);
+  p->xv = knob("COMBO_XV", 4);
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;  // fused: 24.7 ms vs 15.5 + 5.7 split (512^3)
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
   if (n3 >= 8) {
@@ -452,11 +452,32 @@ void launch_xgamma(combo_ctx* c, int kind) {
         k<<<unsigned(gr), p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g, ntiles, p.pxbuf);
       } else {
         dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.dims[1]), 3u);
-        if (p.xv == 3 && p.rxT <= 256) {
+        if (p.xv == 4 && p.rxT <= 256) {
+          const size_t smem = size_t(2 * (p.dims[0] + p.dims[0] / 8) * p.rxW) * sizeof(double2);
+          auto go = [&](auto k) {
+            smem_attr(k, smem);
+            k<<<grid, p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+          };
+          if (p.xminb == 3) {
+            if (kind == 0)
+              go(xgamma_v4<L, 0, 3>);
+            else if (kind == 1)
+              go(xgamma_v4<L, 1, 3>);
+            else
+              go(xgamma_v4<L, 2, 3>);
+          } else {
+            if (kind == 0)
+              go(xgamma_v4<L, 0, 2>);
+            else if (kind == 1)
+              go(xgamma_v4<L, 1, 2>);
+            else
+              go(xgamma_v4<L, 2, 2>);
+          }
+        } else if (p.xv == 3 && p.rxT <= 256) {
           auto k = xgamma_v3<L, 256, 2>;
           smem_attr(k, p.rxsmem);
           k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
-        } else if (p.xv >= 3) {
+        } else if (p.xv == 3 || p.xv >= 5) {
           auto k = xgamma_v3<L, 512, 1>;
           smem_attr(k, p.rxsmem);
           k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);

@@ -518,6 +518,148 @@ static __global__ void __launch_bounds__(MAXT, MINB)
   }
 }
 
+// ------------------------------------------------ X + Gamma, rank-1 variant
+// Gamma^0 row rg at k is rank one: tau_J <- gr_J s / den with
+// s = sum_L conj(gr_L) tau_L (green.cpp:67-130). In all three schemes the
+// column symbols gr_1, gr_2 factor as (per-k1 scalar a) x (per-(k2, k3)
+// constant), so along an x line
+//   s(k1)  = conj(gr_0(k1)) T_0(k1) + conj(a(k1)) FFT_x(e_1 t_1 + e_2 t_2)
+//   out_J  = o_J IFFT_x(a s / den)   for J = 1, 2
+// with e_J = conj(o_J) constant on the line. The pass therefore transforms
+// two channels forward and two back instead of three: 1/3 less FP64 work,
+// 16 instead of 24 complex registers and two shared-memory channel regions
+// (three blocks per SM). Equal to gamma_row up to floating-point
+// reassociation (linearity of the DFT).
+__device__ __forceinline__ double drcp(double d) {
+  // MUFU seed + three Newton steps (no slow-path call in the hot loop)
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // conj(a) b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+template <int KIND>
+struct RankCol {
+  double2 o1, o2;  // output column factors (row's gr_1, gr_2 without a(k1))
+  double2 c0;      // rotated: a2 a3
+  double d12;      // |o1|^2 + |o2|^2
+  bool zero;       // continuous: the column lies on a Nyquist plane
+};
+
+template <int KIND>
+__device__ __forceinline__ RankCol<KIND> rank_col(const GreenTables& G, int row, int64_t k2, int64_t k3, int64_t n2,
+                                                  int64_t n3) {
+  RankCol<KIND> c;
+  c.c0 = make_double2(0.0, 0.0);
+  c.zero = false;
+  if constexpr (KIND == 0) {
+    c.o1 = make_double2(G.xi[1][k2], 0.0);
+    c.o2 = make_double2(G.xi[2][k3], 0.0);
+    c.zero = 2 * k2 == n2 || 2 * k3 == n3;
+  } else if constexpr (KIND == 1) {
+    const double2 a2 = __ldg(G.avg[1] + k2), a3 = __ldg(G.avg[2] + k3);
+    c.c0 = cmul(a2, a3);
+    c.o1 = cmul(__ldg(G.fwd[1] + k2), a3);
+    c.o2 = cmul(__ldg(G.fwd[2] + k3), a2);
+  } else {
+    const double2 f1 = __ldg(G.fwd[1] + k2), f2 = __ldg(G.fwd[2] + k3);
+    c.o1 = row == 1 ? f1 : make_double2(-f1.x, f1.y);
+    c.o2 = row == 2 ? f2 : make_double2(-f2.x, f2.y);
+  }
+  c.d12 = (c.o1.x * c.o1.x + c.o1.y * c.o1.y) + (c.o2.x * c.o2.x + c.o2.y * c.o2.y);
+  return c;
+}
+
+// (T0, U) at k1 -> (out_0, H) with out_1,2 = o_1,2 H
+template <int KIND>
+__device__ __forceinline__ void rank_gamma(const GreenTables& G, const RankCol<KIND>& c, int row, int64_t k1,
+                                           int64_t n1, double2& t0, double2& u) {
+  double2 g0, a;
+  if constexpr (KIND == 0) {
+    if (c.zero || 2 * k1 == n1) {
+      t0 = u = make_double2(0.0, 0.0);
+      return;
+    }
+    g0 = make_double2(__ldg(G.xi[0] + k1), 0.0);  // real form of g = i xi
+    a = make_double2(1.0, 0.0);
+  } else if constexpr (KIND == 1) {
+    g0 = cmul(__ldg(G.fwd[0] + k1), c.c0);
+    a = __ldg(G.avg[0] + k1);
+  } else {
+    const double2 f0 = __ldg(G.fwd[0] + k1);
+    g0 = row == 0 ? f0 : make_double2(-f0.x, f0.y);
+    a = make_double2(1.0, 0.0);
+  }
+  const double aa = a.x * a.x + a.y * a.y;
+  const double den = (g0.x * g0.x + g0.y * g0.y) + aa * c.d12;
+  if (den == 0.0) {
+    t0 = u = make_double2(0.0, 0.0);
+    return;
+  }
+  const double2 s0 = cmulc(g0, t0), s1 = cmulc(a, u);
+  const double r = drcp(den);
+  const double2 h = make_double2((s0.x + s1.x) * r, (s0.y + s1.y) * r);
+  t0 = cmul(g0, h);
+  u = cmul(a, h);
+}
+
+template <int L, int KIND, int MINB>
+static __global__ void __launch_bounds__(256, MINB)
+    xgamma_v4(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G) {
+  constexpr int N = 1 << L;
+  extern __shared__ double2 sm[];
+  const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
+  const int w = min(W, int(sv.n3c) - kc0);
+  const int line = threadIdx.x % W, u = threadIdx.x / W;
+  const bool active = line < w && u < N / 8;
+  const int64_t plane = sv.n1 * sv.n2 * sv.n3p;
+  const int64_t rowstride = sv.n2 * sv.n3p;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.n3p + kc0 + line;
+  const RankCol<KIND> col = rank_col<KIND>(G, rg, j, kc0 + line, sv.n2, sv.n3);
+  double2 v[2][8];
+  if (active) {
+    double2 t1[8], t2[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t o = int64_t(rr_first_pos<L, false>(u, q)) * rowstride;
+      v[0][q] = base[o];
+      t1[q] = base[plane + o];
+      t2[q] = base[2 * plane + o];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double2 a = cmulc(col.o1, t1[q]), b = cmulc(col.o2, t2[q]);
+      v[1][q] = make_double2(a.x + b.x, a.y + b.y);
+    }
+  }
+  const int chs = (N + N / 8) * W;
+  auto addr = [&](int ch, int pos) { return ch * chs + pad8(pos) * W + line; };
+  rr_stages<L, false, false, 0, 2>(v, u, active, sm, tw, addr);
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) rank_gamma<KIND>(G, col, rg, rr_final_pos<L, false>(u, q), sv.n1, v[0][q], v[1][q]);
+  }
+  rr_stages<L, true, true, 0, 2>(v, u, active, sm, tw, addr);
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t o = int64_t(rr_final_pos<L, true>(u, q)) * rowstride;
+      base[o] = v[0][q];
+      base[plane + o] = cmul(col.o1, v[1][q]);
+      base[2 * plane + o] = cmul(col.o2, v[1][q]);
+    }
+  }
+}
+
 // plain X pass (raw FFT test entry point)
 template <int L, bool INV>
 static __global__ void __launch_bounds__(512, 2) xpass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
