@@ -95,6 +95,7 @@ struct FftPlan {
   bool pipe_z = false, pipe_y = false, pipe_x = false;
   int xv = 4;  // X+Gamma kernel variant (2 = xgamma_rr, 3 = xgamma_v3, 4 = rank-1 xgamma_v4)
   int xminb = 2;  // xgamma_v4 blocks per SM (launch bound)
+  int yminb = 2;  // y pass blocks per SM (launch bound)
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
   DBuf<double2> spec;
   combo_dev::SpecView sv() const {

@@ -283,9 +283,20 @@ double spec_bytes(const combo_ctx* c) {
 }
 
 // ------------------------------------------------------ launch helpers
+// COMBO_CARVEOUT: shared-memory carveout percentage (default: driver's choice)
+int carveout_knob() {
+  static const int v = [] {
+    const char* s = std::getenv("COMBO_CARVEOUT");
+    return s ? std::atoi(s) : -1;
+  }();
+  return v;
+}
+
 template <class K>
 void smem_attr(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) COMBO_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  if (bytes > 0 && carveout_knob() >= 0)
+    COMBO_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_knob()));
 }
 
 // compile-time line length: log2(n) for powers of two <= 1024, else generic
@@ -421,9 +432,16 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
         k<<<unsigned(g), p.ryT, smem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW, ntiles, p.pybuf);
       } else {
         dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.dims[0]), unsigned(ncomp));
-        auto k = ypass_rr<L, INV>;
-        smem_attr(k, p.rysmem);
-        k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
+        auto go = [&](auto k) {
+          smem_attr(k, p.rysmem);
+          k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
+        };
+        if (p.yminb == 5 && p.ryT <= 256)
+          go(ypass_rr<L, INV, 256, 5>);
+        else if (p.yminb == 6 && p.ryT <= 256)
+          go(ypass_rr<L, INV, 256, 6>);
+        else
+          go(ypass_rr<L, INV>);
       }
     } else {
       dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.dims[0]), unsigned(ncomp));
@@ -452,27 +470,26 @@ void launch_xgamma(combo_ctx* c, int kind) {
         k<<<unsigned(gr), p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g, ntiles, p.pxbuf);
       } else {
         dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.dims[1]), 3u);
-        if (p.xv == 4 && p.rxT <= 256) {
+        if (p.xv == 4) {
           const size_t smem = size_t(2 * (p.dims[0] + p.dims[0] / 8) * p.rxW) * sizeof(double2);
           auto go = [&](auto k) {
             smem_attr(k, smem);
             k<<<grid, p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
           };
-          if (p.xminb == 3) {
+          auto by_kind = [&](auto k0, auto k1, auto k2) {
             if (kind == 0)
-              go(xgamma_v4<L, 0, 3>);
+              go(k0);
             else if (kind == 1)
-              go(xgamma_v4<L, 1, 3>);
+              go(k1);
             else
-              go(xgamma_v4<L, 2, 3>);
-          } else {
-            if (kind == 0)
-              go(xgamma_v4<L, 0, 2>);
-            else if (kind == 1)
-              go(xgamma_v4<L, 1, 2>);
-            else
-              go(xgamma_v4<L, 2, 2>);
-          }
+              go(k2);
+          };
+          if (p.rxT > 256)
+            by_kind(xgamma_v4<L, 0, 512, 1>, xgamma_v4<L, 1, 512, 1>, xgamma_v4<L, 2, 512, 1>);
+          else if (p.xminb == 3)
+            by_kind(xgamma_v4<L, 0, 256, 3>, xgamma_v4<L, 1, 256, 3>, xgamma_v4<L, 2, 256, 3>);
+          else
+            by_kind(xgamma_v4<L, 0, 256, 2>, xgamma_v4<L, 1, 256, 2>, xgamma_v4<L, 2, 256, 2>);
         } else if (p.xv == 3 && p.rxT <= 256) {
           auto k = xgamma_v3<L, 256, 2>;
           smem_attr(k, p.rxsmem);

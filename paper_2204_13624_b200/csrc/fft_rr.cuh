@@ -28,22 +28,47 @@ struct Seq {
   }
 };
 
-// butterflies of one stage on the 8 register values of a channel
-template <int N, int R, int P, bool INV>
-__device__ __forceinline__ void rr_bfly(double2 (&v)[8], int u, const double2* __restrict__ tw) {
-  constexpr int B = 8 / R;
+// Base twiddles of one stage: w^(k TS) per butterfly (k = t mod P); the
+// R - 1 twiddles of a butterfly are its powers, formed in registers (depth-3
+// product tree, <= 4 ulp) so a stage issues one 16-byte L1 load per
+// butterfly instead of R - 1, and the load can be hoisted above the
+// preceding exchange barrier.
+template <int N, int R, int P>
+__device__ __forceinline__ void rr_twload(double2 (&w)[8 / R], int u, const double2* __restrict__ tw) {
   constexpr int TS = N / (P * R);
 #pragma unroll
-  for (int q = 0; q < B; ++q) {
-    const int t = u + q * (N / 8);
-    const int k = t & (P - 1);
+  for (int q = 0; q < 8 / R; ++q) {
     if constexpr (P > 1) {
+      const int k = (u + q * (N / 8)) & (P - 1);
+      w[q] = __ldg(tw + k * TS);
+    } else {
+      w[q] = make_double2(1.0, 0.0);
+    }
+  }
+}
+
+// butterflies of one stage on the 8 register values of a channel
+template <int N, int R, int P, bool INV>
+__device__ __forceinline__ void rr_bfly(double2 (&v)[8], const double2 (&w)[8 / R]) {
+  constexpr int B = 8 / R;
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        double2 w = __ldg(tw + r * k * TS);
-        if (INV) w.y = -w.y;
-        v[q * R + r] = cmul(v[q * R + r], w);
+  for (int q = 0; q < B; ++q) {
+    if constexpr (P > 1) {
+      double2 p[8];
+      p[1] = w[q];
+      if (INV) p[1].y = -p[1].y;
+      if constexpr (R >= 4) {
+        p[2] = cmul(p[1], p[1]);
+        p[3] = cmul(p[2], p[1]);
       }
+      if constexpr (R == 8) {
+        p[4] = cmul(p[2], p[2]);
+        p[5] = cmul(p[4], p[1]);
+        p[6] = cmul(p[3], p[3]);
+        p[7] = cmul(p[4], p[3]);
+      }
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[q * R + r] = cmul(v[q * R + r], p[r]);
     }
     dftR<R, INV>(&v[q * R]);
   }
@@ -66,37 +91,52 @@ __device__ __forceinline__ int rr_in(int u, int q, int r) {
 // the shared-memory slot of channel ch at line position pos (per thread's
 // line). All threads of the block must call this (barriers inside).
 template <int L, bool INV, bool REV, int S, int C, class Addr>
+__device__ __forceinline__ void rr_stages_w(double2 (&v)[C][8], int u, bool active, double2* sm,
+                                            const double2* __restrict__ tw, const Addr& addr,
+                                            const double2 (&w)[8 / Seq<L, REV>::R(S)]) {
+  using Q = Seq<L, REV>;
+  constexpr int N = Q::N, R = Q::R(S), P = Q::P(S);
+  if (active) {
+#pragma unroll
+    for (int ch = 0; ch < C; ++ch) rr_bfly<N, R, P, INV>(v[ch], w);
+  }
+  if constexpr (S + 1 < Q::NS) {
+    constexpr int R2 = Q::R(S + 1), P2 = Q::P(S + 1);
+    double2 wn[8 / R2];
+    rr_twload<N, R2, P2>(wn, u, tw);  // latency overlaps the exchange
+    if (active) {
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+        for (int q = 0; q < 8 / R; ++q)
+#pragma unroll
+          for (int r = 0; r < R; ++r) sm[addr(ch, rr_out<N, R, P>(u, q, r))] = v[ch][q * R + r];
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int ch = 0; ch < C; ++ch)
+#pragma unroll
+        for (int q = 0; q < 8 / R2; ++q)
+#pragma unroll
+          for (int r = 0; r < R2; ++r) v[ch][q * R2 + r] = sm[addr(ch, rr_in<N, R2>(u, q, r))];
+    }
+    __syncthreads();
+    rr_stages_w<L, INV, REV, S + 1, C>(v, u, active, sm, tw, addr, wn);
+  }
+}
+
+// Stages S.. of the transform on C channels held in v. addr(ch, pos) gives
+// the shared-memory slot of channel ch at line position pos (per thread's
+// line). All threads of the block must call this (barriers inside).
+template <int L, bool INV, bool REV, int S, int C, class Addr>
 __device__ __forceinline__ void rr_stages(double2 (&v)[C][8], int u, bool active, double2* sm,
                                           const double2* __restrict__ tw, const Addr& addr) {
   using Q = Seq<L, REV>;
   if constexpr (S < Q::NS) {
-    constexpr int N = Q::N, R = Q::R(S), P = Q::P(S);
-    if (active) {
-#pragma unroll
-      for (int ch = 0; ch < C; ++ch) rr_bfly<N, R, P, INV>(v[ch], u, tw);
-    }
-    if constexpr (S + 1 < Q::NS) {
-      constexpr int R2 = Q::R(S + 1);
-      if (active) {
-#pragma unroll
-        for (int ch = 0; ch < C; ++ch)
-#pragma unroll
-          for (int q = 0; q < 8 / R; ++q)
-#pragma unroll
-            for (int r = 0; r < R; ++r) sm[addr(ch, rr_out<N, R, P>(u, q, r))] = v[ch][q * R + r];
-      }
-      __syncthreads();
-      if (active) {
-#pragma unroll
-        for (int ch = 0; ch < C; ++ch)
-#pragma unroll
-          for (int q = 0; q < 8 / R2; ++q)
-#pragma unroll
-            for (int r = 0; r < R2; ++r) v[ch][q * R2 + r] = sm[addr(ch, rr_in<N, R2>(u, q, r))];
-      }
-      __syncthreads();
-      rr_stages<L, INV, REV, S + 1, C>(v, u, active, sm, tw, addr);
-    }
+    double2 w[8 / Q::R(S)];
+    rr_twload<Q::N, Q::R(S), Q::P(S)>(w, u, tw);
+    rr_stages_w<L, INV, REV, S, C>(v, u, active, sm, tw, addr, w);
   }
 }
 
@@ -316,8 +356,8 @@ static __global__ void __launch_bounds__(512, 2)
 
 // ------------------------------------------------------------------ Y pass
 // W columns (lines) per block, thread -> (line = tid % W, u = tid / W)
-template <int L, bool INV>
-static __global__ void __launch_bounds__(512, 2) ypass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
+template <int L, bool INV, int MAXT = 512, int MINB = 2>
+static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
   constexpr int N = 1 << L;
   extern __shared__ double2 sm[];
   const int c = blockIdx.z, i = blockIdx.y, kc0 = blockIdx.x * W;
@@ -612,8 +652,8 @@ __device__ __forceinline__ void rank_gamma(const GreenTables& G, const RankCol<K
   u = cmul(a, h);
 }
 
-template <int L, int KIND, int MINB>
-static __global__ void __launch_bounds__(256, MINB)
+template <int L, int KIND, int MAXT, int MINB>
+static __global__ void __launch_bounds__(MAXT, MINB)
     xgamma_v4(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G) {
   constexpr int N = 1 << L;
   extern __shared__ double2 sm[];
