@@ -96,6 +96,8 @@ struct FftPlan {
   int xv = 4;  // X+Gamma kernel variant (2 = xgamma_rr, 3 = xgamma_v3, 4 = rank-1 xgamma_v4)
   int xminb = 2;  // xgamma_v4 blocks per SM (launch bound)
   int yminb = 2;  // y pass blocks per SM (launch bound)
+  bool y2 = false;  // y pass with two columns per thread (ypass_rr2)
+  bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
   DBuf<double2> spec;
   combo_dev::SpecView sv() const {
@@ -106,6 +108,9 @@ struct FftPlan {
     s.n3 = dims[2];
     s.n3c = n3c;
     s.n3p = n3p;
+    s.plane = dims[0] * dims[1] * n3p;
+    s.si = swap ? n3p : dims[1] * n3p;
+    s.sj = swap ? dims[0] * n3p : n3p;
     return s;
   }
 };

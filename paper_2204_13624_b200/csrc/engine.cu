@@ -193,7 +193,7 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
       return Lz;
     };
     int64_t Lz = lines_for(512);
-    if (knob("COMBO_ZLINES", 0) > 0) Lz = knob("COMBO_ZLINES", 0);
+    if (knob("COMBO_ZLINES", 0) > 0) Lz = std::min<int64_t>(knob("COMBO_ZLINES", 0), combo_dev::kMaxZRows / 9);
     p->rzL = int(Lz);
     const int64_t np = (9 * Lz + 1) / 2;
     p->rzT = int((np * tl + 31) / 32 * 32);
@@ -204,10 +204,13 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     const int64_t ls = n3 + n3 / 8, lsd = (ls + 1) & ~int64_t(1);
     p->pzbuf = int(std::max({np * ls, (9 * Lz * lsd + 1) / 2, 9 * Lz * p->n3p}));
   }
+  p->swap = knob("COMBO_SWAP", 0) != 0;  // j-major rows: x 5.5 ms, y 4.7 ms; i-major: x 6.3, y 4.2 (512^3)
   if (d[1] >= 8) {
     int Wy = int(std::min<int64_t>(8, p->n3c));
-    // 256-thread tiles measured faster than 512 at n2 = 512 (4.5 vs 4.8 ms)
-    while (Wy > 1 && Wy * (d[1] / 8) > 256) Wy /= 2;
+    // i-major rows: 256-thread tiles measured faster than 512 at n2 = 512
+    // (4.5 vs 4.8 ms); j-major rows: y lines take the long stride and want
+    // 128-byte row segments (W = 8)
+    while (Wy > 1 && Wy * (d[1] / 8) > (p->swap ? 512 : 256)) Wy /= 2;
     if (knob("COMBO_YW", 0) > 0) Wy = knob("COMBO_YW", 0);
     p->ryW = Wy;
     p->ryT = int(std::max<int64_t>(32, (Wy * (d[1] / 8) + 31) / 32 * 32));
@@ -294,7 +297,8 @@ int carveout_knob() {
 
 template <class K>
 void smem_attr(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) COMBO_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  // always opt in: static + dynamic above 48 KB needs the attribute too
+  if (bytes > 0) COMBO_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
   if (bytes > 0 && carveout_knob() >= 0)
     COMBO_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_knob()));
 }
@@ -436,7 +440,12 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
           smem_attr(k, p.rysmem);
           k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
         };
-        if (p.yminb == 5 && p.ryT <= 256)
+        if (p.y2 && p.ryW >= 2 && p.ryW % 2 == 0 && p.ryW * (p.dims[1] / 8) / 2 <= 256) {
+          auto k = ypass_rr2<L, INV>;
+          smem_attr(k, p.rysmem);
+          k<<<grid, std::max(32, int(p.ryW * (p.dims[1] / 8) / 2 + 31) / 32 * 32), p.rysmem, c->stream>>>(
+              p.sv(), p.ax[1].tw.p, p.ryW);
+        } else if (p.yminb == 5 && p.ryT <= 256)
           go(ypass_rr<L, INV, 256, 5>);
         else if (p.yminb == 6 && p.ryT <= 256)
           go(ypass_rr<L, INV, 256, 6>);
@@ -1617,10 +1626,15 @@ int combo_fft_forward(combo_ctx* c, const int64_t dims[3], int ncomp, const doub
     launch_zfwd(c, ProdLoad9{c->scratch[0].p, N});
     launch_y<false>(c);
     launch_x_plain<false>(c);
-    // unpadded interleaved copy out
-    const size_t rows = size_t(ncomp * p.dims[0] * p.dims[1]);
-    COMBO_CK(cudaMemcpy2DAsync(out, size_t(p.n3c) * 16, p.spec.p, size_t(p.n3p) * 16, size_t(p.n3c) * 16, rows,
-                               mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+    // unpadded [c][i][j][k] copy out, one (c, i) plane of rows at a time
+    const SpecView sv = p.sv();
+    for (int64_t cc = 0; cc < ncomp; ++cc)
+      for (int64_t i = 0; i < p.dims[0]; ++i)
+        COMBO_CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(out) + size_t((cc * p.dims[0] + i) * p.dims[1] * p.n3c) * 16,
+                                   size_t(p.n3c) * 16, sv.spec + cc * sv.plane + i * sv.si, size_t(sv.sj) * 16,
+                                   size_t(p.n3c) * 16, size_t(p.dims[1]),
+                                   mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                   c->stream));
     COMBO_CK(cudaStreamSynchronize(c->stream));
   });
 }

@@ -262,9 +262,19 @@ __device__ void block_reduce_store(double (&acc)[NRED], double* partials, int64_
 }
 
 // ---------------------------------------------------------------- passes
+// Half spectrum: rows of n3p complex, row (c, i, j) at c plane + i si + j sj.
+// The engine stores j-major rows (si = n3p, sj = n1 n3p) so that the x lines
+// read by the three-channel X+Gamma pass are 4 KB apart (DRAM-page friendly)
+// and the one-channel Y pass takes the long stride with 128-byte segments.
 struct SpecView {
-  double2* spec;  // [9][n1][n2][n3p]
+  double2* spec;
   int64_t n1, n2, n3, n3c, n3p;
+  int64_t si, sj, plane;
+  // offset of the row of component c on z-line `line` = i n2 + j
+  __host__ __device__ __forceinline__ int64_t zrow(int64_t c, int64_t line) const {
+    const int64_t i = line / n2;
+    return c * plane + i * si + (line - i * n2) * sj;
+  }
 };
 
 template <int LOG2N>
@@ -312,13 +322,13 @@ static __global__ void __launch_bounds__(kMaxFftThreads)
     const double2 zm = sm[pp * ls + (k == 0 ? 0 : n - k)];
     int rl = 2 * pp;
     int li = rl / 9, c = rl - 9 * li;
-    sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k] =
+    sv.spec[sv.zrow(c, line0 + li) + k] =
         make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
     ++rl;
     if (rl < nreal) {
       li = rl / 9;
       c = rl - 9 * li;
-      sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k] =
+      sv.spec[sv.zrow(c, line0 + li) + k] =
           make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
     }
   }
@@ -341,13 +351,13 @@ static __global__ void __launch_bounds__(kMaxFftThreads)
     const int pp = t / nc, k = t - pp * nc;
     int rl = 2 * pp;
     int li = rl / 9, c = rl - 9 * li;
-    double2 xa = sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k];
+    double2 xa = sv.spec[sv.zrow(c, line0 + li) + k];
     double2 xb = make_double2(0.0, 0.0);
     ++rl;
     if (rl < nreal) {
       li = rl / 9;
       c = rl - 9 * li;
-      xb = sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k];
+      xb = sv.spec[sv.zrow(c, line0 + li) + k];
     }
     const bool selfconj = (k == 0) || (2 * k == n);
     if (selfconj) {
@@ -385,16 +395,16 @@ static __global__ void __launch_bounds__(kMaxFftThreads) ypass_kernel(SpecView s
   const int n2 = line_len<LOG2N>(ax);
   const int c = blockIdx.z, i = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
-  double2* base = sv.spec + ((int64_t(c) * sv.n1 + i) * sv.n2) * sv.n3p + kc0;
+  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(i) * sv.si + kc0;
   for (int t = threadIdx.x; t < n2 * W; t += blockDim.x) {
     const int j = t / W, col = t - j * W;
-    if (col < w) sm[t] = base[int64_t(j) * sv.n3p + col];
+    if (col < w) sm[t] = base[int64_t(j) * sv.sj + col];
   }
   __syncthreads();
   fft_lines<LOG2N, INV, true>(sm, ax, W, W, 1);
   for (int t = threadIdx.x; t < n2 * W; t += blockDim.x) {
     const int j = t / W, col = t - j * W;
-    if (col < w) base[int64_t(j) * sv.n3p + col] = sm[t];
+    if (col < w) base[int64_t(j) * sv.sj + col] = sm[t];
   }
 }
 
@@ -460,11 +470,11 @@ static __global__ void __launch_bounds__(kMaxFftThreads) xgamma_kernel(SpecView 
   const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
   const int W3 = 3 * W;
-  const int64_t plane = sv.n1 * sv.n2 * sv.n3p;  // component stride
-  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.n3p + kc0;
+  const int64_t plane = sv.plane;  // component stride
+  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.sj + kc0;
   for (int t = threadIdx.x; t < n1 * W3; t += blockDim.x) {
     const int i = t / W3, rem = t - i * W3, cc = rem / W, col = rem - cc * W;
-    if (col < w) sm[t] = base[int64_t(cc) * plane + int64_t(i) * sv.n2 * sv.n3p + col];
+    if (col < w) sm[t] = base[int64_t(cc) * plane + int64_t(i) * sv.si + col];
   }
   __syncthreads();
   fft_lines<LOG2N, false, true>(sm, ax, W3, W3, 1);
@@ -483,7 +493,7 @@ static __global__ void __launch_bounds__(kMaxFftThreads) xgamma_kernel(SpecView 
   fft_lines<LOG2N, true, true>(sm, ax, W3, W3, 1);
   for (int t = threadIdx.x; t < n1 * W3; t += blockDim.x) {
     const int i = t / W3, rem = t - i * W3, cc = rem / W, col = rem - cc * W;
-    if (col < w) base[int64_t(cc) * plane + int64_t(i) * sv.n2 * sv.n3p + col] = sm[t];
+    if (col < w) base[int64_t(cc) * plane + int64_t(i) * sv.si + col] = sm[t];
   }
 }
 
@@ -494,16 +504,16 @@ static __global__ void __launch_bounds__(kMaxFftThreads) xpass_kernel(SpecView s
   const int n1 = line_len<LOG2N>(ax);
   const int c = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
-  double2* base = sv.spec + int64_t(c) * sv.n1 * sv.n2 * sv.n3p + int64_t(j) * sv.n3p + kc0;
+  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(j) * sv.sj + kc0;
   for (int t = threadIdx.x; t < n1 * W; t += blockDim.x) {
     const int i = t / W, col = t - i * W;
-    if (col < w) sm[t] = base[int64_t(i) * sv.n2 * sv.n3p + col];
+    if (col < w) sm[t] = base[int64_t(i) * sv.si + col];
   }
   __syncthreads();
   fft_lines<LOG2N, INV, true>(sm, ax, W, W, 1);
   for (int t = threadIdx.x; t < n1 * W; t += blockDim.x) {
     const int i = t / W, col = t - i * W;
-    if (col < w) base[int64_t(i) * sv.n2 * sv.n3p + col] = sm[t];
+    if (col < w) base[int64_t(i) * sv.si + col] = sm[t];
   }
 }
 

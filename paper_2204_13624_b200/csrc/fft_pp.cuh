@@ -37,14 +37,14 @@ static __global__ void __launch_bounds__(512, 1) ypass_pp(SpecView sv, const dou
     const int64_t rest = tile / ntk;
     const int64_t i = rest % sv.n1, c = rest / sv.n1;
     w = min(W, int(sv.n3c) - kt * W);
-    return sv.spec + ((c * sv.n1 + i) * sv.n2) * sv.n3p + int64_t(kt) * W;
+    return sv.spec + c * sv.plane + i * sv.si + int64_t(kt) * W;
   };
   auto prefetch = [&](double2* buf, int64_t tile) {
     int w;
     const double2* g = base_of(tile, w);
     for (int idx = threadIdx.x; idx < N * W; idx += blockDim.x) {
       const int row = idx / W, col = idx - row * W;
-      if (col < w) cp_async16(buf + pad8(row) * W + col, g + int64_t(row) * sv.n3p + col);
+      if (col < w) cp_async16(buf + pad8(row) * W + col, g + int64_t(row) * sv.sj + col);
     }
     cp_async_commit();
   };
@@ -73,7 +73,7 @@ static __global__ void __launch_bounds__(512, 1) ypass_pp(SpecView sv, const dou
     rr_stages<L, INV, false, 0, 1>(v, u, active, buf, tw, addr);
     if (active) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) g[int64_t(rr_final_pos<L, false>(u, q)) * sv.n3p + line] = v[0][q];
+      for (int q = 0; q < 8; ++q) g[int64_t(rr_final_pos<L, false>(u, q)) * sv.sj + line] = v[0][q];
     }
     __syncthreads();
   }
@@ -88,8 +88,8 @@ static __global__ void __launch_bounds__(256, 1) xgamma_pp(SpecView sv, const do
   extern __shared__ double2 sm[];
   const int ntk = int((sv.n3c + W - 1) / W);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
-  const int64_t plane = sv.n1 * sv.n2 * sv.n3p;
-  const int64_t rowstride = sv.n2 * sv.n3p;
+  const int64_t plane = sv.plane;
+  const int64_t rowstride = sv.si;
   const int chs = (N + N / 8) * W;
   auto base_of = [&](int64_t tile, int& w, int64_t& j, int& rg, int& kc0) {
     const int kt = int(tile % ntk);
@@ -98,7 +98,7 @@ static __global__ void __launch_bounds__(256, 1) xgamma_pp(SpecView sv, const do
     rg = int(rest / sv.n2);
     kc0 = kt * W;
     w = min(W, int(sv.n3c) - kc0);
-    return sv.spec + int64_t(3 * rg) * plane + j * sv.n3p + kc0;
+    return sv.spec + int64_t(3 * rg) * plane + j * sv.sj + kc0;
   };
   auto prefetch = [&](double2* buf, int64_t tile) {
     int w, rg, kc0;
@@ -228,13 +228,13 @@ static __global__ void __launch_bounds__(384, 2)
       const double2 zm = buf[pp * LS + pad8(k == 0 ? 0 : N - k)];
       int rl = 2 * pp;
       int li = rl / 9, c = rl - 9 * li;
-      sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k] =
+      sv.spec[sv.zrow(c, line0 + li) + k] =
           make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
       ++rl;
       if (rl < nreal) {
         li = rl / 9;
         c = rl - 9 * li;
-        sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k] =
+        sv.spec[sv.zrow(c, line0 + li) + k] =
             make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
       }
     }
@@ -266,7 +266,7 @@ static __global__ void __launch_bounds__(384, 2) zinv_pp(SpecView sv, const doub
     for (int idx = threadIdx.x; idx < 9 * nl * nc; idx += blockDim.x) {
       const int rl = idx / nc, k = idx - rl * nc;
       const int li = rl / 9, c = rl - 9 * li;
-      cp_async16(buf + rl * int(sv.n3p) + k, sv.spec + (int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k);
+      cp_async16(buf + rl * int(sv.n3p) + k, sv.spec + sv.zrow(c, line0 + li) + k);
     }
     cp_async_commit();
   };

@@ -210,6 +210,7 @@ __device__ void group_reduce_store(double (&sc)[NSC > 0 ? NSC : 1], double pa, d
 }
 
 // ------------------------------------------------------------------ Z pass
+constexpr int kMaxZRows = 1024;  // 9 x lines per block (T <= 512 bounds it)
 // Pairs of real lines (comp c of z-line l, enumerated rl = 9 l + c) are packed
 // as one complex line; T = npair * N/8 threads, thread -> (pair, u).
 template <class Prod, int L>
@@ -259,6 +260,10 @@ static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
       v[0][i].y = hasb ? prod.comp(cb, cellb + e) : 0.0;
     }
   }
+  // spectrum row offsets of the block's real lines (read after the barriers
+  // inside rr_stages)
+  __shared__ int64_t zr[kMaxZRows];
+  for (int t = threadIdx.x; t < nreal; t += blockDim.x) zr[t] = sv.zrow(t % 9, line0 + t / 9);
   auto addr = [&](int, int pos) { return p * LS + pad8(pos); };
   rr_stages<L, false, false, 0, 1>(v, u, active, sm, tw, addr);
   // natural order to smem, then split the pair into two half spectra
@@ -268,21 +273,17 @@ static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
   }
   __syncthreads();
   const int nc = int(sv.n3c);
-  for (int t = threadIdx.x; t < npair * nc; t += blockDim.x) {
-    const int pp = t / nc, k = t - pp * nc;
+  // warp-aligned k ranges per pair: the 8-lane phases of the 16-byte shared
+  // loads then never straddle a pad slot (bank conflicts otherwise)
+  const int ncr = (nc + 31) & ~31;
+  for (int t = threadIdx.x; t < npair * ncr; t += blockDim.x) {
+    const int pp = t / ncr, k = t - pp * ncr;
+    if (k >= nc) continue;
     const double2 zk = sm[pp * LS + pad8(k)];
     const double2 zm = sm[pp * LS + pad8(k == 0 ? 0 : N - k)];
-    int rl = 2 * pp;
-    int li = rl / 9, c = rl - 9 * li;
-    sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k] =
-        make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    ++rl;
-    if (rl < nreal) {
-      li = rl / 9;
-      c = rl - 9 * li;
-      sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k] =
-          make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-    }
+    const int rl = 2 * pp;
+    sv.spec[zr[rl] + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    if (rl + 1 < nreal) sv.spec[zr[rl + 1] + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
   }
 }
 
@@ -298,20 +299,19 @@ static __global__ void __launch_bounds__(512, 2)
   const int nreal = 9 * nlines;
   const int npair = (nreal + 1) >> 1;
   const int nc = int(sv.n3c);
+  const int ncr = (nc + 31) & ~31;  // warp-aligned k ranges (see zfwd_rr)
+  __shared__ int64_t zr[kMaxZRows];
+  for (int t = threadIdx.x; t < nreal; t += blockDim.x) zr[t] = sv.zrow(t % 9, line0 + t / 9);
+  __syncthreads();
   // Hermitian completion of the pair (halfcomplex c2r: DC/Nyquist imaginary
   // parts ignored) into natural-order smem lines
-  for (int t = threadIdx.x; t < npair * nc; t += blockDim.x) {
-    const int pp = t / nc, k = t - pp * nc;
-    int rl = 2 * pp;
-    int li = rl / 9, c = rl - 9 * li;
-    double2 xa = sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k];
-    double2 xb = make_double2(0.0, 0.0);
-    ++rl;
-    if (rl < nreal) {
-      li = rl / 9;
-      c = rl - 9 * li;
-      xb = sv.spec[(int64_t(c) * nlines_tot + line0 + li) * sv.n3p + k];
-    }
+  for (int t = threadIdx.x; t < npair * ncr; t += blockDim.x) {
+    const int pp = t / ncr, k = t - pp * ncr;
+    if (k >= nc) continue;
+    const int rl = 2 * pp;
+    double2 xa = sv.spec[zr[rl] + k];
+    const double2 xb0 = make_double2(0.0, 0.0);
+    double2 xb = rl + 1 < nreal ? sv.spec[zr[rl + 1] + k] : xb0;
     const bool selfconj = (k == 0) || (2 * k == N);
     if (selfconj) {
       xa.y = 0.0;
@@ -364,17 +364,51 @@ static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  double2* base = sv.spec + ((int64_t(c) * sv.n1 + i) * sv.n2) * sv.n3p + kc0 + line;
+  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(i) * sv.si + kc0 + line;
   double2 v[1][8];
   if (active) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[0][q] = base[int64_t(rr_first_pos<L, false>(u, q)) * sv.n3p];
+    for (int q = 0; q < 8; ++q) v[0][q] = base[int64_t(rr_first_pos<L, false>(u, q)) * sv.sj];
   }
   auto addr = [&](int, int pos) { return pad8(pos) * W + line; };
   rr_stages<L, INV, false, 0, 1>(v, u, active, sm, tw, addr);
   if (active) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) base[int64_t(rr_final_pos<L, false>(u, q)) * sv.n3p] = v[0][q];
+    for (int q = 0; q < 8; ++q) base[int64_t(rr_final_pos<L, false>(u, q)) * sv.sj] = v[0][q];
+  }
+}
+
+// Y pass with two columns per thread (columns line and line + W/2): twice the
+// independent loads per thread at the same warp count, so W = 8 tiles (128-
+// byte row segments) run with 256 threads.
+template <int L, bool INV>
+static __global__ void __launch_bounds__(256, 2) ypass_rr2(SpecView sv, const double2* __restrict__ tw, int W) {
+  constexpr int N = 1 << L;
+  extern __shared__ double2 sm[];
+  const int W2 = W >> 1;
+  const int c = blockIdx.z, i = blockIdx.y, kc0 = blockIdx.x * W;
+  const int w = min(W, int(sv.n3c) - kc0);
+  const int line = threadIdx.x % W2, u = threadIdx.x / W2;
+  const bool active = u < N / 8;
+  const bool on[2] = {line < w, line + W2 < w};
+  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(i) * sv.si + kc0 + line;
+  double2 v[2][8];
+  if (active) {
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch)
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        v[ch][q] = on[ch] ? base[int64_t(rr_first_pos<L, false>(u, q)) * sv.sj + ch * W2] : make_double2(0.0, 0.0);
+  }
+  auto addr = [&](int ch, int pos) { return pad8(pos) * W + ch * W2 + line; };
+  rr_stages<L, INV, false, 0, 2>(v, u, active, sm, tw, addr);
+  if (active) {
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch)
+      if (on[ch]) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) base[int64_t(rr_final_pos<L, false>(u, q)) * sv.sj + ch * W2] = v[ch][q];
+      }
   }
 }
 
@@ -389,9 +423,9 @@ static __global__ void __launch_bounds__(256, 2)
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  const int64_t plane = sv.n1 * sv.n2 * sv.n3p;
-  const int64_t rowstride = sv.n2 * sv.n3p;
-  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.n3p + kc0 + line;
+  const int64_t plane = sv.plane;
+  const int64_t rowstride = sv.si;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.sj + kc0 + line;
   double2 v[3][8];
   if (active) {
 #pragma unroll
@@ -525,9 +559,9 @@ static __global__ void __launch_bounds__(MAXT, MINB)
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  const int64_t plane = sv.n1 * sv.n2 * sv.n3p;
-  const int64_t rowstride = sv.n2 * sv.n3p;
-  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.n3p + kc0 + line;
+  const int64_t plane = sv.plane;
+  const int64_t rowstride = sv.si;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.sj + kc0 + line;
   double2 v[3][8];
   if (active) {
 #pragma unroll
@@ -661,9 +695,9 @@ static __global__ void __launch_bounds__(MAXT, MINB)
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  const int64_t plane = sv.n1 * sv.n2 * sv.n3p;
-  const int64_t rowstride = sv.n2 * sv.n3p;
-  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.n3p + kc0 + line;
+  const int64_t plane = sv.plane;
+  const int64_t rowstride = sv.si;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.sj + kc0 + line;
   const RankCol<KIND> col = rank_col<KIND>(G, rg, j, kc0 + line, sv.n2, sv.n3);
   double2 v[2][8];
   if (active) {
@@ -709,8 +743,8 @@ static __global__ void __launch_bounds__(512, 2) xpass_rr(SpecView sv, const dou
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  const int64_t rowstride = sv.n2 * sv.n3p;
-  double2* base = sv.spec + int64_t(c) * sv.n1 * rowstride + int64_t(j) * sv.n3p + kc0 + line;
+  const int64_t rowstride = sv.si;
+  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(j) * sv.sj + kc0 + line;
   double2 v[1][8];
   if (active) {
 #pragma unroll
