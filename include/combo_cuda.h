@@ -164,6 +164,26 @@ int combo_normals(combo_ctx* ctx, const uint8_t* img, const int64_t dims[3], con
                   int min_interface_voxels, double* normal3, uint8_t* flags, combo_normal_stats* stats,
                   int mem);
 
+/* ------------------------------------------------------- slab decomposition */
+/* Multi-GPU layout of SURVEY.md 8e (the reference is single-process OpenMP,
+ * parallel.hpp:19; these calls have no reference counterpart): R ranks own
+ * contiguous slabs of n1/R planes along axis 0 (R must divide n1 and n2);
+ * the FFT transposes slab <-> pencil with one all-to-all per direction and
+ * all scalar reductions combine per-chunk partials in global order, so every
+ * result is bitwise independent of R. Call before combo_bind_materials /
+ * combo_set_grid; bind / solve / project then take whole-grid arrays.
+ *
+ * combo_ctx_set_virtual_ranks: R ranks hosted by this context on its device
+ *   (test harness for the decomposition; outputs gathered in slab order).
+ * combo_ctx_set_ranks: one rank per process; nccl_id = 128 bytes from
+ *   combo_nccl_unique_id on rank 0, broadcast by the caller. F_out / P_out
+ *   / project outputs then hold this rank's slab [9][n1/R * n2 * n3]. */
+int combo_nccl_unique_id(void* nccl_id128);
+int combo_ctx_set_virtual_ranks(combo_ctx* ctx, int nranks);
+int combo_ctx_set_ranks(combo_ctx* ctx, int nranks, int rank, const void* nccl_id128);
+int combo_ctx_ranks(const combo_ctx* ctx, int* nranks, int* rank, int* local_ranks, int64_t* i0,
+                    int64_t* ni);
+
 /* ------------------------------------------------------------------ binding */
 /* SimGrid (field.hpp:16-28) for operator calls that need no materials
  * (combo_project); combo_bind_materials sets it too. */

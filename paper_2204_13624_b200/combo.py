@@ -92,6 +92,10 @@ SIGNATURES = {
     "combo_normals": (C.c_int, [_VP, _VP, _I64, _D, _I64, _VP, C.c_int, C.c_int, C.c_int, _VP, _VP,
                                 C.POINTER(NormalStats), C.c_int]),
     "combo_set_grid": (C.c_int, [_VP, _I64, _D]),
+    "combo_nccl_unique_id": (C.c_int, [_VP]),
+    "combo_ctx_set_virtual_ranks": (C.c_int, [_VP, C.c_int]),
+    "combo_ctx_set_ranks": (C.c_int, [_VP, C.c_int, C.c_int, _VP]),
+    "combo_ctx_ranks": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "combo_bind_materials": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, C.POINTER(Law), C.POINTER(Law), C.c_int,
                                        C.POINTER(LamOpts), C.c_int]),
     "combo_composite_cells": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
@@ -339,6 +343,36 @@ class Context:
                                          C.byref(st), _mem(img, kind)))
         return n3.reshape(nb, 3), flags, (st.composite, st.degenerate_fallbacks, st.too_few_fallbacks)
 
+    # ------------------------------------------------ slab decomposition
+    def set_virtual_ranks(self, nranks):
+        """Host `nranks` slab ranks on this context's device (SURVEY.md 8e);
+        bind / solve / project keep whole-grid arrays and are bitwise
+        independent of the rank count."""
+        self._check(self.L.combo_ctx_set_virtual_ranks(self.h, int(nranks)))
+
+    def nccl_unique_id(self):
+        buf = (C.c_char * 128)()
+        self._check(self.L.combo_nccl_unique_id(buf), ctx=None)
+        return bytes(buf)
+
+    def set_ranks(self, nranks, rank, nccl_id=None):
+        """One rank per process (NCCL): nccl_id from rank 0's nccl_unique_id(),
+        broadcast by the caller (e.g. torch.distributed.broadcast_object_list)."""
+        buf = None
+        if nccl_id is not None:
+            buf = (C.c_char * 128).from_buffer_copy(bytes(nccl_id))
+        self._check(self.L.combo_ctx_set_ranks(self.h, int(nranks), int(rank), buf))
+
+    def ranks(self):
+        n, r, loc = C.c_int(), C.c_int(), C.c_int()
+        i0, ni = C.c_int64(), C.c_int64()
+        self._check(self.L.combo_ctx_ranks(self.h, C.byref(n), C.byref(r), C.byref(loc), C.byref(i0), C.byref(ni)))
+        return {"nranks": n.value, "rank": r.value, "local_ranks": loc.value, "i0": i0.value, "ni": ni.value}
+
+    def _out_fraction(self):
+        rk = self.ranks()
+        return rk["local_ranks"] / rk["nranks"]
+
     # --------------------------------------------------------- operators
     def set_grid(self, dims, lengths=(1.0, 1.0, 1.0)):
         self._check(self.L.combo_set_grid(self.h, _i64(dims), _f64(lengths)))
@@ -348,7 +382,7 @@ class Context:
         if dims is not None:
             self.set_grid(dims, lengths)
         f = _f64(field).ravel()
-        out = np.zeros_like(f)
+        out = np.zeros(int(round(f.size * self._out_fraction())))
         self._check(self.L.combo_project(self.h, GREEN[kind] if isinstance(kind, str) else int(kind), _ptr(f),
                                          _ptr(out), MEM_HOST))
         return out
@@ -451,8 +485,9 @@ class CellMaterials:
         """solve (solver.cpp:286-346) -> dict(f, p, pbar, report). f_out /
         p_out may be caller buffers (numpy / pinned or CUDA tensors)."""
         cfg = cfg or SolverConfig(**kw)
-        F = f_out if f_out is not None else (np.zeros(9 * self.n) if want_fields else None)
-        P = p_out if p_out is not None else (np.zeros(9 * self.n) if want_fields else None)
+        nloc = int(round(self.n * self.ctx._out_fraction()))  # this process's slabs
+        F = f_out if f_out is not None else (np.zeros(9 * nloc) if want_fields else None)
+        P = p_out if p_out is not None else (np.zeros(9 * nloc) if want_fields else None)
         pbar = np.zeros(9)
         rep = C.c_void_p()
         cc = cfg.c()

@@ -40,6 +40,20 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
   ~DBuf() { release(); }
   void release() {
     if (p) cudaFree(p);
@@ -96,10 +110,16 @@ struct FftPlan {
   int xv = 4;  // X+Gamma kernel variant (2 = xgamma_rr, 3 = xgamma_v3, 4 = rank-1 xgamma_v4)
   int xminb = 2;  // xgamma_v4 blocks per SM (launch bound)
   int yminb = 2;  // y pass blocks per SM (launch bound)
+  int mvminb = 1;  // CG matvec blocks per SM (launch bound)
   bool y2 = false;  // y pass with two columns per thread (ypass_rr2)
   bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
-  DBuf<double2> spec;
+  // slab decomposition (R ranks, this plan's rank q): planes [i0, i0 + ni)
+  // on the slab side, k2 in [j0, j0 + nj) on the pencil side
+  int R = 1, q = 0;
+  int64_t ni = 0, nj = 0, i0 = 0, j0 = 0;
+  DBuf<double2> spec;   // slab side (z, y passes)
+  DBuf<double2> specB;  // pencil side (x pass + Gamma), R > 1 only
   combo_dev::SpecView sv() const {
     combo_dev::SpecView s;
     s.spec = spec.p;
@@ -108,9 +128,20 @@ struct FftPlan {
     s.n3 = dims[2];
     s.n3c = n3c;
     s.n3p = n3p;
-    s.plane = dims[0] * dims[1] * n3p;
+    s.blocked = R > 1 ? 1 : 0;
+    s.ni = ni;
+    s.nj = nj;
+    s.i0 = i0;
+    s.j0 = j0;
+    s.blk = 9 * ni * nj * n3p;
+    s.cs = R > 1 ? ni * nj * n3p : dims[0] * dims[1] * n3p;
     s.si = swap ? n3p : dims[1] * n3p;
     s.sj = swap ? dims[0] * n3p : n3p;
+    return s;
+  }
+  combo_dev::SpecView svB() const {
+    combo_dev::SpecView s = sv();
+    if (R > 1) s.spec = specB.p;
     return s;
   }
 };
@@ -154,7 +185,20 @@ struct combo_ctx {
   bool has_grid = false;
   std::array<int64_t, 3> dims{0, 0, 0};
   std::array<double, 3> lengths{1, 1, 1};
-  int64_t N = 0;
+  int64_t N = 0;   // cells of this context's slab
+  int64_t Ng = 0;  // cells of the whole grid
+
+  // slab decomposition (combo_ctx_set_ranks / combo_ctx_set_virtual_ranks):
+  // R ranks along axis 0, this context is rank q. Emulated ranks live in one
+  // process on one device as member contexts of the leader (vm) and share
+  // its stream; with one rank per process the exchange runs over NCCL.
+  int R = 1, q = 0;
+  combo_ctx* lead = nullptr;                   // group leader (nullptr: self)
+  std::vector<std::unique_ptr<combo_ctx>> vm;  // emulated ranks 1..R-1
+  void* nccl = nullptr;                        // ncclComm_t (one rank per process)
+  bool own_stream = true;
+  combo_host::DBuf<double> gpart;              // leader: block partials of all ranks
+  combo_host::DBuf<combo_dev::Stats> gstats;   // NCCL: laminate stats of all ranks
   std::unique_ptr<combo_host::FftPlan> plan;
 
   // materials (combo_bind_materials)
@@ -206,6 +250,18 @@ struct combo_ctx {
 };
 
 namespace combo_host {
+// operator-level entry points act on one slab
+inline void require_single(const combo_ctx* c) {
+  if (c->R > 1)
+    throw ComboError(COMBO_ERR_STATE, "operator-level entry points need a single-slab context (R = 1)");
+}
+// comm.cu: NCCL (loaded at run time) for one-rank-per-process decompositions
+void nccl_init(combo_ctx* c, int nranks, int rank, const void* uid);
+void nccl_destroy(combo_ctx* c);
+void nccl_allgather_inplace(combo_ctx* c, double* buf, size_t count_per_rank);
+void nccl_allreduce_u64(combo_ctx* c, const unsigned long long* in, unsigned long long* out, size_t n, bool max);
+void nccl_alltoall_blocks(combo_ctx* c, const double2* src, double2* dst, size_t blk);
+void nccl_allreduce_sum(combo_ctx* c, double* buf, size_t n);
 // engine.cu
 void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths);
 int ew_grid(int64_t n);
@@ -223,7 +279,7 @@ void dfmg_matvec(combo_ctx* c, const double* fin, const combo_dev::Shift9& sh, c
 // kernel tags for the profiler
 enum ProfTag {
   kTagSweep, kTagMatvec, kTagZfwd, kTagYfwd, kTagXGamma, kTagYinv, kTagZinv, kTagCgUpdate, kTagTrial,
-  kTagMaterialize, kTagReduce, kTagOther, kTagMvZfwd, kNumTags
+  kTagMaterialize, kTagReduce, kTagOther, kTagMvZfwd, kTagExchange, kNumTags
 };
 // RAII: records CUDA events around the launches in its scope when enabled
 struct ProfScope {

@@ -342,6 +342,7 @@ extern "C" {
 int combo_dfmg_stress(combo_ctx* c, const double* F, double* P, combo_sweep_stats* st, int mem) {
   return guarded(c, [&] {
     if (!c->bound) throw ComboError(COMBO_ERR_STATE, "materials not bound (combo_bind_materials)");
+    require_single(c);
     ensure_scratch(c);
     const double* f = stage_in(c, F, mem, 0);
     double* p = stage_out(c, P, mem, 1);
@@ -364,6 +365,7 @@ int combo_dfmg_stress(combo_ctx* c, const double* F, double* P, combo_sweep_stat
 int combo_dfmg_tangent_matvec(combo_ctx* c, const double* F, const double* x, double* y, int mem) {
   return guarded(c, [&] {
     if (!c->bound) throw ComboError(COMBO_ERR_STATE, "materials not bound (combo_bind_materials)");
+    require_single(c);
     ensure_scratch(c);
     const double* f = stage_in(c, F, mem, 0);
     const double* xx = stage_in(c, x, mem, 1);
@@ -380,6 +382,7 @@ int combo_dfmg_tangent_matvec(combo_ctx* c, const double* F, const double* x, do
 int combo_dfmg_get_warm_starts(combo_ctx* c, double* warm3, int mem) {
   return guarded(c, [&] {
     if (!c->bound) throw ComboError(COMBO_ERR_STATE, "materials not bound (combo_bind_materials)");
+    require_single(c);
     ensure_dfmg(c);
     const int64_t nw = 8 * c->ncomp;
     if (!nw) return;

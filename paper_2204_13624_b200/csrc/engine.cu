@@ -141,14 +141,30 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   }
   const std::array<int64_t, 3> d{dims[0], dims[1], dims[2]};
   const std::array<double, 3> l{lengths[0], lengths[1], lengths[2]};
+  const int R = c->R;
+  if (R > 1 && (d[0] % R != 0 || d[1] % R != 0))
+    throw ComboError(COMBO_ERR_BAD_SHAPE, "slab decomposition: the rank count must divide n1 and n2");
   c->has_grid = true;
   c->dims = d;
   c->lengths = l;
-  c->N = d[0] * d[1] * d[2];
-  if (c->plan && c->plan->dims == d && c->plan->lengths == l) return;
+  c->Ng = d[0] * d[1] * d[2];
+  c->N = (d[0] / R) * d[1] * d[2];
+  if (c->plan && c->plan->dims == d && c->plan->lengths == l && c->plan->R == R && c->plan->q == c->q) return;
   auto p = std::make_unique<FftPlan>();
   p->dims = d;
   p->lengths = l;
+  p->R = R;
+  p->q = c->q;
+  p->ni = d[0] / R;
+  p->nj = d[1] / R;
+  p->i0 = c->q * p->ni;
+  p->j0 = c->q * p->nj;
+  // z-line blocks never straddle a plane (decomposition-invariant partials)
+  auto divisor_le = [&](int64_t L) {
+    L = std::max<int64_t>(1, std::min(L, d[1]));
+    while (d[1] % L != 0) --L;
+    return L;
+  };
   for (int a = 0; a < 3; ++a) build_axis(p->ax[a], int(d[a]));
   p->n3c = d[2] / 2 + 1;
   p->n3p = (p->n3c + 7) / 8 * 8;
@@ -156,6 +172,7 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   const int64_t n3 = d[2];
   int64_t L = std::max<int64_t>(1, 1024 / n3);
   while (L > 1 && ((9 * L + 1) / 2) * n3 > 6144) --L;
+  L = divisor_le(L);
   p->zL = int(L);
   p->zls = int(n3);
   const int64_t npair = (9 * L + 1) / 2;
@@ -194,11 +211,12 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     };
     int64_t Lz = lines_for(512);
     if (knob("COMBO_ZLINES", 0) > 0) Lz = std::min<int64_t>(knob("COMBO_ZLINES", 0), combo_dev::kMaxZRows / 9);
+    Lz = divisor_le(Lz);
     p->rzL = int(Lz);
     const int64_t np = (9 * Lz + 1) / 2;
     p->rzT = int((np * tl + 31) / 32 * 32);
     // fused matvec producer: <= 384 threads (register budget of the NH code)
-    p->rzLc = int(lines_for(384));
+    p->rzLc = int(divisor_le(lines_for(384)));
     p->rzTc = int((((9 * p->rzLc + 1) / 2) * tl + 31) / 32 * 32);
     p->rzsmem = size_t(np * (n3 + n3 / 8)) * sizeof(double2);
     const int64_t ls = n3 + n3 / 8, lsd = (ls + 1) & ~int64_t(1);
@@ -226,7 +244,14 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     p->rxsmem = size_t(3 * (d[0] + d[0] / 8) * Wx) * sizeof(double2);
     p->pxbuf = int(3 * (d[0] + d[0] / 8) * Wx);
   }
-  p->spec.alloc(size_t(9 * d[0] * d[1] * p->n3p));
+  p->spec.alloc(size_t(9 * p->ni * d[1] * p->n3p));
+  if (R > 1) {
+    p->specB.alloc(size_t(9 * p->ni * d[1] * p->n3p));
+    // pipelined / older X variants are single-slab only
+    p->pipe_x = p->pipe_y = p->pipe_z = false;
+    p->xv = 4;
+    p->swap = false;
+  }
   c->plan = std::move(p);
 }
 
@@ -245,13 +270,86 @@ void reduce_partials(combo_ctx* c, int64_t nblocks, int nred, int slot) {
 }
 
 void fetch_results(combo_ctx* c) {
+  const Stats* st = c->dstats.p;
+  if (c->nccl && c->R > 1) {
+    // laminate statistics of all ranks: sums and the maximum iteration count
+    c->gstats.alloc(1);
+    nccl_allreduce_u64(c, reinterpret_cast<const unsigned long long*>(c->dstats.p),
+                       reinterpret_cast<unsigned long long*>(c->gstats.p), 3, false);
+    nccl_allreduce_u64(c, &c->dstats.p->iter_max, &c->gstats.p->iter_max, 1, true);
+    st = c->gstats.p;
+  }
   COMBO_CK(cudaMemcpyAsync(c->hres, c->dres.p, 64 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  COMBO_CK(cudaMemcpyAsync(c->hres + 64, c->dstats.p, sizeof(Stats), cudaMemcpyDeviceToHost, c->stream));
+  COMBO_CK(cudaMemcpyAsync(c->hres + 64, st, sizeof(Stats), cudaMemcpyDeviceToHost, c->stream));
   COMBO_CK(cudaStreamSynchronize(c->stream));
 }
 
 void ensure_partials(combo_ctx* c, int64_t count) {
   if (c->partials.n < size_t(count)) c->partials.alloc(size_t(count));
+}
+
+// ------------------------------------------------- slab decomposition
+combo_ctx* leader(combo_ctx* c) { return c->lead ? c->lead : c; }
+
+std::vector<combo_ctx*> members(combo_ctx* c) {
+  std::vector<combo_ctx*> v{c};
+  for (auto& m : c->vm) v.push_back(m.get());
+  return v;
+}
+
+// Block partials of rank q for a launch of nb blocks x nred values per rank:
+// [global block][nred] in the leader's buffer (all ranks' blocks, rank order)
+double* part_ptr(combo_ctx* c, int64_t nb, int nred) {
+  combo_ctx* L = leader(c);
+  const size_t need = size_t(c->R) * size_t(nb) * size_t(nred);
+  if (L->gpart.n < need) L->gpart.alloc(need);
+  return L->gpart.p + size_t(c->q) * size_t(nb) * size_t(nred);
+}
+
+Stats* stats_ptr(combo_ctx* c) { return leader(c)->dstats.p; }
+
+// fixed-order combination of every rank's block partials -> dres[slot..]
+void group_reduce(combo_ctx* c, int64_t nb, int nred, int slot) {
+  combo_ctx* L = leader(c);
+  if (L->nccl && L->R > 1) nccl_allgather_inplace(L, L->gpart.p, size_t(nb) * size_t(nred));
+  ProfScope ps(L, kTagReduce, double(L->R) * double(nb) * nred * 8.0);
+  k_reduce_partials<<<nred, 1024, 0, L->stream>>>(L->gpart.p, int64_t(L->R) * nb, nred, L->dres.p + slot);
+  ++L->launches;
+  COMBO_CK(cudaGetLastError());
+}
+
+// chunked launches (decomposition-invariant partials, kernels.cuh)
+Chunks chunks_of(const combo_ctx* c) {
+  Chunks k;
+  k.plane = c->dims[1] * c->dims[2];
+  k.cpp = int((k.plane + kChunk - 1) / kChunk);
+  return k;
+}
+int64_t chunk_blocks(const combo_ctx* c) { return (c->N / (c->dims[1] * c->dims[2])) * chunks_of(c).cpp; }
+
+// slab <-> pencil transpose of the spectrum (SpecView): block s of rank q's
+// slab side is block q of rank s's pencil side
+void exchange(combo_ctx* c, bool to_pencil) {
+  combo_ctx* L = leader(c);
+  if (L->R == 1) return;
+  const FftPlan& p0 = *L->plan;
+  const size_t blk = size_t(9 * p0.ni * p0.nj * p0.n3p);
+  ProfScope ps(L, kTagExchange, 2.0 * double(L->R - 1) * double(blk) * 16.0 * (L->nccl ? 1.0 : double(L->R)));
+  if (L->nccl) {
+    double2* src = to_pencil ? L->plan->spec.p : L->plan->specB.p;
+    double2* dst = to_pencil ? L->plan->specB.p : L->plan->spec.p;
+    nccl_alltoall_blocks(L, src, dst, blk);
+    return;
+  }
+  auto ms = members(L);
+  for (int q = 0; q < L->R; ++q)
+    for (int s = 0; s < L->R; ++s) {
+      const double2* src = to_pencil ? ms[size_t(q)]->plan->spec.p + size_t(s) * blk
+                                     : ms[size_t(s)]->plan->specB.p + size_t(q) * blk;
+      double2* dst = to_pencil ? ms[size_t(s)]->plan->specB.p + size_t(q) * blk
+                               : ms[size_t(q)]->plan->spec.p + size_t(s) * blk;
+      COMBO_CK(cudaMemcpyAsync(dst, src, blk * sizeof(double2), cudaMemcpyDeviceToDevice, L->stream));
+    }
 }
 
 // ------------------------------------------------------------- profiler
@@ -267,10 +365,11 @@ cudaEvent_t pool_event(combo_ctx* c) {
   return e;
 }
 const char* kTagNames[kNumTags] = {"sweep",  "matvec",    "zfwd",      "yfwd",   "xgamma", "yinv",
-                                   "zinv",   "cg_update", "trial",     "materialize", "reduce", "other", "matvec_zfwd"};
+                                   "zinv",   "cg_update", "trial",     "materialize", "reduce", "other", "matvec_zfwd", "exchange"};
 }  // namespace
 
-ProfScope::ProfScope(combo_ctx* ctx, int tag, double bytes) : c(ctx) {
+// emulated ranks record into the leader's profile (they share its stream)
+ProfScope::ProfScope(combo_ctx* ctx, int tag, double bytes) : c(ctx->lead ? ctx->lead : ctx) {
   if (!c->prof_on) return;
   combo_ctx::ProfRec r{tag, pool_event(c), pool_event(c), bytes};
   COMBO_CK(cudaEventRecord(r.a, c->stream));
@@ -282,7 +381,7 @@ ProfScope::~ProfScope() {
 }
 
 double spec_bytes(const combo_ctx* c) {
-  return 9.0 * double(c->plan->dims[0] * c->plan->dims[1] * c->plan->n3c) * 16.0;
+  return 9.0 * double(c->plan->ni * c->plan->dims[1] * c->plan->n3c) * 16.0;
 }
 
 // ------------------------------------------------------ launch helpers
@@ -348,7 +447,7 @@ int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      const int64_t ntiles = (p.dims[0] * p.dims[1] + p.rzL - 1) / p.rzL;
+      const int64_t ntiles = (p.ni * p.dims[1] + p.rzL - 1) / p.rzL;
       bool piped = false;
       if constexpr (!Prod::CELL) {
         if (p.pipe_z) {
@@ -362,18 +461,18 @@ int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
       }
       if (!piped) {
         const int lz = Prod::CELL ? p.rzLc : p.rzL;
-        nb = (p.dims[0] * p.dims[1] + lz - 1) / lz;
+        nb = (p.ni * p.dims[1] + lz - 1) / lz;
         auto k = zfwd_rr<Prod, L>;
         smem_attr(k, p.rzsmem);
         k<<<unsigned(nb), Prod::CELL ? p.rzTc : p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, lz, prod,
-                                                                            c->partials.p);
+                                                                            nullptr);
       }
     } else {
-      nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
-      if (Prod::NRED) ensure_partials(c, nb * Prod::NRED);
+      nb = (p.ni * p.dims[1] + p.zL - 1) / p.zL;
+      double* part = Prod::NRED ? part_ptr(c, nb, Prod::NRED) : nullptr;
       auto k = zfwd_kernel<Prod, L>;
       smem_attr(k, p.zsmem);
-      k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, prod, c->partials.p);
+      k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, prod, part);
     }
   });
   ++c->launches;
@@ -385,34 +484,33 @@ template <class Cons>
 int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
   FftPlan& p = *c->plan;
   int64_t nb = 0;
-  const double scale = 1.0 / double(c->N);
+  const double scale = 1.0 / double(c->Ng);
   ProfScope ps(c, kTagZinv, spec_bytes(c) + 72.0 * double(c->N) * Cons::FIELDS);
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      const int64_t ntiles = (p.dims[0] * p.dims[1] + p.rzL - 1) / p.rzL;
+      const int64_t ntiles = (p.ni * p.dims[1] + p.rzL - 1) / p.rzL;
       if (p.pipe_z) {
         const size_t smem = size_t(2 * p.pzbuf) * sizeof(double2);
         auto k = zinv_pp<Cons, L>;
         smem_attr(k, smem);
         nb = pp_grid(c, k, p.rzT, smem, ntiles);
-        if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
+        double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
         k<<<unsigned(nb), p.rzT, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, ntiles, p.pzbuf, scale, cons,
-                                                    c->partials.p);
+                                                    part);
       } else {
         nb = ntiles;
-        if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
+        double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
         auto k = zinv_rr<Cons, L>;
         smem_attr(k, p.rzsmem);
-        k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, c->partials.p);
+        k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
       }
     } else {
-      nb = (p.dims[0] * p.dims[1] + p.zL - 1) / p.zL;
-      if (Cons::NRED) ensure_partials(c, nb * Cons::NRED);
+      nb = (p.ni * p.dims[1] + p.zL - 1) / p.zL;
+      double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
       auto k = zinv_kernel<Cons, L>;
       smem_attr(k, p.zsmem);
-      k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, scale, cons,
-                                                    c->partials.p);
+      k<<<unsigned(nb), p.zT, p.zsmem, c->stream>>>(p.sv(), p.ax[2].view(), p.zL, p.zls, scale, cons, part);
     }
   });
   ++c->launches;
@@ -428,14 +526,14 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
       if (p.pipe_y) {
-        const int64_t ntiles = ((p.n3c + p.ryW - 1) / p.ryW) * p.dims[0] * ncomp;
+        const int64_t ntiles = ((p.n3c + p.ryW - 1) / p.ryW) * p.ni * ncomp;
         const size_t smem = size_t(2 * p.pybuf) * sizeof(double2);
         auto k = ypass_pp<L, INV>;
         smem_attr(k, smem);
         const int g = pp_grid(c, k, p.ryT, smem, ntiles);
         k<<<unsigned(g), p.ryT, smem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW, ntiles, p.pybuf);
       } else {
-        dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.dims[0]), unsigned(ncomp));
+        dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.ni), unsigned(ncomp));
         auto go = [&](auto k) {
           smem_attr(k, p.rysmem);
           k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
@@ -453,7 +551,7 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
           go(ypass_rr<L, INV>);
       }
     } else {
-      dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.dims[0]), unsigned(ncomp));
+      dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_kernel<L, INV>;
       smem_attr(k, p.ysmem);
       k<<<grid, p.yT, p.ysmem, c->stream>>>(p.sv(), p.ax[1].view(), p.yW);
@@ -471,19 +569,19 @@ void launch_xgamma(combo_ctx* c, int kind) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
       if (p.pipe_x) {
-        const int64_t ntiles = ((p.n3c + p.rxW - 1) / p.rxW) * p.dims[1] * 3;
+        const int64_t ntiles = ((p.n3c + p.rxW - 1) / p.rxW) * p.nj * 3;
         const size_t smem = size_t(2 * p.pxbuf) * sizeof(double2);
         auto k = xgamma_pp<L>;
         smem_attr(k, smem);
         const int gr = pp_grid(c, k, p.rxT, smem, ntiles);
-        k<<<unsigned(gr), p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g, ntiles, p.pxbuf);
+        k<<<unsigned(gr), p.rxT, smem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g, ntiles, p.pxbuf);
       } else {
-        dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.dims[1]), 3u);
+        dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), 3u);
         if (p.xv == 4) {
           const size_t smem = size_t(2 * (p.dims[0] + p.dims[0] / 8) * p.rxW) * sizeof(double2);
           auto go = [&](auto k) {
             smem_attr(k, smem);
-            k<<<grid, p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+            k<<<grid, p.rxT, smem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
           };
           auto by_kind = [&](auto k0, auto k1, auto k2) {
             if (kind == 0)
@@ -502,22 +600,22 @@ void launch_xgamma(combo_ctx* c, int kind) {
         } else if (p.xv == 3 && p.rxT <= 256) {
           auto k = xgamma_v3<L, 256, 2>;
           smem_attr(k, p.rxsmem);
-          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
         } else if (p.xv == 3 || p.xv >= 5) {
           auto k = xgamma_v3<L, 512, 1>;
           smem_attr(k, p.rxsmem);
-          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
         } else {
           auto k = xgamma_rr<L>;
           smem_attr(k, p.rxsmem);
-          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW, g);
+          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
         }
       }
     } else {
-      dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 3u);
+      dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.nj), 3u);
       auto k = xgamma_kernel<L>;
       smem_attr(k, p.xsmem);
-      k<<<grid, p.xT, p.xsmem, c->stream>>>(p.sv(), p.ax[0].view(), p.xW, g);
+      k<<<grid, p.xT, p.xsmem, c->stream>>>(p.svB(), p.ax[0].view(), p.xW, g);
     }
   });
   ++c->launches;
@@ -530,54 +628,73 @@ void launch_x_plain(combo_ctx* c) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
       const size_t smem = size_t((p.dims[0] + p.dims[0] / 8) * p.rxW) * sizeof(double2);
-      dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.dims[1]), 9u);
+      dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), 9u);
       auto k = xpass_rr<L, INV>;
       smem_attr(k, smem);
-      k<<<grid, p.rxT, smem, c->stream>>>(p.sv(), p.ax[0].tw.p, p.rxW);
+      k<<<grid, p.rxT, smem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW);
     } else {
       // plain x pass: x tile geometry with a single component per block
       const size_t smem = size_t(p.dims[0] * p.xW) * sizeof(double2);
-      dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.dims[1]), 9u);
+      dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.nj), 9u);
       auto k = xpass_kernel<L, INV>;
       smem_attr(k, smem);
-      k<<<grid, pick_threads(p.dims[0] * p.xW), smem, c->stream>>>(p.sv(), p.ax[0].view(), p.xW);
+      k<<<grid, pick_threads(p.dims[0] * p.xW), smem, c->stream>>>(p.svB(), p.ax[0].view(), p.xW);
     }
   });
   ++c->launches;
   COMBO_CK(cudaGetLastError());
 }
 // Projection Pi(tau) = alpha Gamma^0 tau (green.cpp:133-151) with fused
-// producer / consumer. Returns the partial-block counts via nbp / nbc.
+// producer / consumer, over every rank hosted by the leader c: prodf(k) /
+// consf(k) build member k's producer and consumer. z and y passes run on
+// the slabs, the spectrum is transposed to pencils for the x pass + Gamma
+// and back; the consumer's partials of all ranks are combined in global
+// block order into dres[slot_cons..].
+template <class PF, class CF>
+void project_group(combo_ctx* c, int kind, PF&& prodf, CF&& consf, int slot_cons, double prod_bytes = 0.0) {
+  const auto ms = members(c);
+  using Prod = std::decay_t<decltype(prodf(size_t(0)))>;
+  using Cons = std::decay_t<decltype(consf(size_t(0)))>;
+  static_assert(Prod::NRED == 0, "producer reductions are not combined across ranks");
+  for (size_t k = 0; k < ms.size(); ++k) launch_zfwd(ms[k], prodf(k), prod_bytes);
+  for (auto* m : ms) launch_y<false>(m);
+  exchange(c, true);
+  for (auto* m : ms) launch_xgamma(m, kind);
+  exchange(c, false);
+  for (auto* m : ms) launch_y<true>(m);
+  int64_t nbc = 0;
+  for (size_t k = 0; k < ms.size(); ++k) nbc = launch_zinv(ms[k], consf(k));
+  if (Cons::NRED) group_reduce(c, nbc, Cons::NRED, slot_cons);
+}
+
+// single-slab form (operator-level entry points, DFMG)
 template <class Prod, class Cons>
-void project_fused(combo_ctx* c, int kind, const Prod& prod, const Cons& cons, int slot_prod, int slot_cons,
-                   double prod_bytes = 0.0) {
-  const int64_t nbp = launch_zfwd(c, prod, prod_bytes);
-  if (Prod::NRED) reduce_partials(c, nbp, Prod::NRED, slot_prod);
-  launch_y<false>(c);
-  launch_xgamma(c, kind);
-  launch_y<true>(c);
-  const int64_t nbc = launch_zinv(c, cons);
-  if (Cons::NRED) reduce_partials(c, nbc, Cons::NRED, slot_cons);
+void project_fused(combo_ctx* c, int kind, const Prod& prod, const Cons& cons, int slot_cons) {
+  if (!c->vm.empty()) throw ComboError(COMBO_ERR_STATE, "project_fused: single slab only");
+  project_group(c, kind, [&](size_t) { return prod; }, [&](size_t) { return cons; }, slot_cons);
 }
 
 void reset_stats(combo_ctx* c) {
-  COMBO_CK(cudaMemsetAsync(c->dstats.p, 0, sizeof(Stats), c->stream));
+  COMBO_CK(cudaMemsetAsync(leader(c)->dstats.p, 0, sizeof(Stats), leader(c)->stream));
 }
 
 // stress sweep: out = P(fin + sh) - alpha (fin + sh); P sums -> slot
-void sweep(combo_ctx* c, const double* fin, const Shift9& sh, double alpha, double* out, bool writeback,
-           int slot) {
-  const int g = ew_grid(c->N);
-  ensure_partials(c, int64_t(g) * 9);
-  {
-    // F read + out write + cid, composite meta (n, c+, c-) and warm r/w
-    ProfScope ps(c, kTagSweep, 148.0 * double(c->N) + 88.0 * double(c->ncomp));
-    k_sweep<<<g, kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, alpha, out, c->N, writeback ? 1 : 0,
-                                             c->dstats.p, c->partials.p);
-  }
+// one rank's part: partials of its chunks, stats into the leader's counters
+void sweep_launch(combo_ctx* c, const double* fin, const Shift9& sh, double alpha, double* out, bool writeback) {
+  const int64_t nb = chunk_blocks(c);
+  double* part = part_ptr(c, nb, 9);
+  // F read + out write + cid, composite meta (n, c+, c-) and warm r/w
+  ProfScope ps(c, kTagSweep, 148.0 * double(c->N) + 88.0 * double(c->ncomp));
+  k_sweep<<<unsigned(nb), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, alpha, out, c->N, chunks_of(c),
+                                                      writeback ? 1 : 0, stats_ptr(c), part);
   ++c->launches;
   COMBO_CK(cudaGetLastError());
-  reduce_partials(c, g, 9, slot);
+}
+
+void sweep(combo_ctx* c, const double* fin, const Shift9& sh, double alpha, double* out, bool writeback,
+           int slot) {
+  sweep_launch(c, fin, sh, alpha, out, writeback);
+  group_reduce(c, chunk_blocks(c), 9, slot);
 }
 
 Shift9 zero_shift() {
@@ -749,24 +866,33 @@ double norm9(const double* m) {
 struct LsBudget {};
 }  // namespace
 
-// Field slots of the solver (9N doubles each), cached on the context.
-struct SolverFields {
-  DBuf<double> f[9];
+// One rank's solver state: the 9N_local field slots (F, F_new/F_trial, x, r,
+// pdir, ap, P or tau, spare residual) of a slab.
+struct SolverRank {
+  combo_ctx* c;
+  int64_t N;
+  DBuf<double> f[8];
 };
 
+// The solver runs every rank hosted by the leader context in lockstep: each
+// field-sized step is launched per rank, scalars are combined across ranks
+// in global block order (group_reduce), the spectrum is transposed inside
+// project_group. With one rank it is the plain single-GPU solver.
 class Solver {
  public:
-  Solver(combo_ctx* c, const combo_solver_cfg& cfg) : c_(c), cfg_(cfg), N_(c->N) {
+  Solver(combo_ctx* c, const combo_solver_cfg& cfg) : c_(c), cfg_(cfg), Ng_(c->Ng) {
     ensure_scratch(c);
-    for (int i = 0; i < 8; ++i) bufs_[i].alloc(size_t(9 * N_));
-    F_ = bufs_[0].p;
-    Fo_ = bufs_[1].p;  // basic: F_new ; newton: F_trial
-    x_ = bufs_[2].p;
-    r_ = bufs_[3].p;
-    pd_ = bufs_[4].p;
-    ap_ = bufs_[5].p;
-    rb_ = bufs_[6].p;
-    bn_ = bufs_[7].p;
+    for (combo_ctx* m : members(c)) {
+      rk_.emplace_back();
+      SolverRank& r = rk_.back();
+      r.c = m;
+      r.N = m->N;
+      for (auto& b : r.f) b.alloc(size_t(9 * r.N));
+    }
+    if (rk_.size() > 1 || c->R > 1) {
+      if (cfg.eval == COMBO_EVAL_DFMG)
+        throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: DFMG needs a single slab (axis-0 halo not implemented)");
+    }
     double lo, hi;
     const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
     spectrum_bounds(c, I, lo, hi);
@@ -775,13 +901,15 @@ class Solver {
   }
 
   void run(const double* fbar_target, combo_report& rep);
-  double* F() { return F_; }
-  Shift9 shiftF() const { return shF_; }
+  double* F(size_t k) { return P(F_, k); }
+  double* scratch(size_t k) { return P(rb_, k); }
+  size_t nranks() const { return rk_.size(); }
   const double* pbar() const { return pbar_; }
-  void final_stress(double* P);
+  void final_stress(const std::vector<double*>& out);
   void materialize();
 
  private:
+  double* P(int slot, size_t k) { return rk_[k].f[slot].p; }
   bool run_step(const double* fbar, combo_host::StepRec& rep);
   bool run_basic(const double* fbar, combo_host::StepRec& rep);
   bool run_newton(const double* fbar, combo_host::StepRec& rep);
@@ -790,12 +918,14 @@ class Solver {
     if (cfg_.max_ls_iterations > 0 && ls_total_ >= cfg_.max_ls_iterations) throw LsBudget{};
     ++ls_total_;
   }
-  // eval_stress (solver.cpp:59-63): per-cell sweep or DFMG
-  void eval_sweep(const double* fin, const Shift9& sh, double alpha, double* out, bool writeback, int slot) {
-    if (cfg_.eval == COMBO_EVAL_DFMG)
-      dfmg_sweep(c_, fin, sh, alpha, out, slot);
-    else
-      sweep(c_, fin, sh, alpha, out, writeback, slot);
+  // eval_stress (solver.cpp:59-63): per-cell sweep or DFMG; P sums -> slot
+  void eval_sweep(int fin, const Shift9& sh, double alpha, int out, bool writeback, int slot) {
+    if (cfg_.eval == COMBO_EVAL_DFMG) {
+      dfmg_sweep(c_, P(fin, 0), sh, alpha, P(out, 0), slot);
+      return;
+    }
+    for (size_t k = 0; k < rk_.size(); ++k) sweep_launch(rk_[k].c, P(fin, k), sh, alpha, P(out, k), writeback);
+    group_reduce(c_, chunk_blocks(c_), 9, slot);
   }
   combo_sweep_stats stats() const {
     const Stats* s = reinterpret_cast<const Stats*>(c_->hres + 64);
@@ -806,42 +936,47 @@ class Solver {
     o.laminate_iter_max = int64_t(s->iter_max);
     return o;
   }
+  // F + shift materialized in place; per-component sums -> slot
+  void materialize_sum(int slot) {
+    const int64_t nb = chunk_blocks(c_);
+    for (auto& r : rk_) {
+      double* part = part_ptr(r.c, nb, 9);
+      ProfScope ps(r.c, kTagMaterialize, 144.0 * double(r.N));
+      k_materialize<<<unsigned(nb), kEwThreads, 0, r.c->stream>>>(r.f[F_].p, shF_, r.N, chunks_of(r.c), part);
+      ++r.c->launches;
+      COMBO_CK(cudaGetLastError());
+    }
+    group_reduce(c_, nb, 9, slot);
+  }
   // pin_mean on F (field.cpp:28-38): materialize pending shift, sum, new shift
   void pin_mean(const double* target) {
-    const int g = ew_grid(N_);
-    ensure_partials(c_, int64_t(g) * 9);
-    {
-      ProfScope ps(c_, kTagMaterialize, 144.0 * double(N_));
-      k_materialize<<<g, kEwThreads, 0, c_->stream>>>(F_, shF_, N_, c_->partials.p);
-    }
-    ++c_->launches;
-    COMBO_CK(cudaGetLastError());
-    reduce_partials(c_, g, 9, 0);
+    materialize_sum(0);
     fetch_results(c_);
-    for (int q = 0; q < 9; ++q) shF_.v[q] = target[q] - c_->hres[q] / double(N_);
+    for (int q = 0; q < 9; ++q) shF_.v[q] = target[q] - c_->hres[q] / double(Ng_);
+  }
+  void copy_all(int dst, int src) {
+    for (auto& r : rk_)
+      COMBO_CK(cudaMemcpyAsync(r.f[dst].p, r.f[src].p, size_t(9 * r.N) * sizeof(double), cudaMemcpyDeviceToDevice,
+                               r.c->stream));
   }
 
- public:
   combo_ctx* c_;
   combo_solver_cfg cfg_;
-  int64_t N_;
-  DBuf<double> bufs_[8];
-  double *F_, *Fo_, *x_, *r_, *pd_, *ap_, *rb_, *bn_;
+  int64_t Ng_;
+  std::vector<SolverRank> rk_;
+  // field slots (indices into SolverRank::f); swaps exchange the indices
+  int F_ = 0, Fo_ = 1, x_ = 2, r_ = 3, pd_ = 4, ap_ = 5, rb_ = 6, bn_ = 7;
   Shift9 shF_;
   double alpha_ = 1.0;
   double stress_floor_;
   double pbar_[9] = {0};
   int64_t ls_total_ = 0;
-  const double* last_eval_ = nullptr;
+  int last_eval_ = -1;
   Shift9 last_eval_shift_;
 };
 
 void Solver::materialize() {
-  const int g = ew_grid(N_);
-  ensure_partials(c_, int64_t(g) * 9);
-  k_materialize<<<g, kEwThreads, 0, c_->stream>>>(F_, shF_, N_, c_->partials.p);
-  ++c_->launches;
-  COMBO_CK(cudaGetLastError());
+  materialize_sum(0);
   shF_ = zero_shift();
 }
 
@@ -856,30 +991,34 @@ bool Solver::run_basic(const double* fbar, combo_host::StepRec& rep) {
     eval_sweep(F_, shF_, alpha_, rb_, true, 0);  // tau = P - alpha F ; P sums -> slot 0
     last_eval_ = F_;
     last_eval_shift_ = shF_;
-    ConsBasic cons;
-    cons.fold = F_;
-    cons.fold_shift = shF_;
-    cons.fnew = Fo_;
-    for (int q = 0; q < 9; ++q) cons.fbar.v[q] = fbar[q];
-    cons.alpha = alpha_;
-    cons.N = N_;
-    ProdLoad9 prod{rb_, N_};
-    project_fused(c_, cfg_.green, prod, cons, 0, 9);  // diff^2 -> 9, F_new sums -> 10..18
+    project_group(
+        c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
+        [&](size_t k) {
+          ConsBasic cons;
+          cons.fold = P(F_, k);
+          cons.fold_shift = shF_;
+          cons.fnew = P(Fo_, k);
+          for (int q = 0; q < 9; ++q) cons.fbar.v[q] = fbar[q];
+          cons.alpha = alpha_;
+          cons.N = rk_[k].N;
+          return cons;
+        },
+        9);  // diff^2 -> 9, F_new sums -> 10..18
     fetch_results(c_);
     rep.sweep = stats();
     if (rep.sweep.inadmissible_cells > 0) return false;
     count_ls();
     ++rep.ls_basic;
-    for (int q = 0; q < 9; ++q) pbar_[q] = c_->hres[q] / double(N_);
+    for (int q = 0; q < 9; ++q) pbar_[q] = c_->hres[q] / double(Ng_);
     rep.pbar_history.push_back({});
     std::memcpy(rep.pbar_history.back().data(), pbar_, sizeof pbar_);
-    const double resid = alpha_ * std::sqrt(c_->hres[9] / double(N_)) / std::max(norm9(pbar_), stress_floor_);
+    const double resid = alpha_ * std::sqrt(c_->hres[9] / double(Ng_)) / std::max(norm9(pbar_), stress_floor_);
     rep.residuals.push_back(resid);
     rep.cg_iters.push_back(0);
     rep.outer_iters = it;
     if (cfg_.verbose) std::printf("  basic it %3d resid %.3e\n", it, resid);
     std::swap(F_, Fo_);
-    for (int q = 0; q < 9; ++q) shF_.v[q] = fbar[q] - c_->hres[10 + q] / double(N_);
+    for (int q = 0; q < 9; ++q) shF_.v[q] = fbar[q] - c_->hres[10 + q] / double(Ng_);
     if (rep.sweep.laminate_failures > 0 && resid <= cfg_.tol_equilibrium) return false;
     if (resid <= cfg_.tol_equilibrium) {
       rep.converged = true;
@@ -892,7 +1031,7 @@ bool Solver::run_basic(const double* fbar, combo_host::StepRec& rep) {
 // cg_solve (solver.cpp:166-200); r holds b on entry, x is zeroed here
 int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::StepRec& rep) {
   breakdown = false;
-  COMBO_CK(cudaMemsetAsync(x_, 0, size_t(9 * N_) * sizeof(double), c_->stream));
+  for (auto& r : rk_) COMBO_CK(cudaMemsetAsync(r.f[x_].p, 0, size_t(9 * r.N) * sizeof(double), r.c->stream));
   double rr = rr0;
   const double bnorm = std::sqrt(rr);
   if (bnorm == 0.0) return 0;
@@ -900,67 +1039,83 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
   // dfmg_tangent_pass, solver.cpp:72-82)
   const bool dfmg = cfg_.eval == COMBO_EVAL_DFMG;
   if (dfmg)
-    dfmg_tangent_prepare(c_, F_, shF_);
+    dfmg_tangent_prepare(c_, P(F_, 0), shF_);
   else
-    comp_tangents(c_, F_, shF_);
+    for (auto& r : rk_) comp_tangents(r.c, r.f[F_].p, shF_);
   int it = 0;
   double beta = 0.0, step_prev = 0.0;
-  const int g = ew_grid(N_);
+  const int64_t nbc = chunk_blocks(c_);
   // x += step * pdir is deferred into the next matvec (which reads pdir
   // anyway); the last pending update is flushed on exit (solver.cpp:186)
+  auto axpy_x = [&](double s) {
+    for (auto& r : rk_) {
+      ProfScope ps(r.c, kTagCgUpdate, 216.0 * double(r.N));
+      k_axpy<<<ew_grid(9 * r.N), kEwThreads, 0, r.c->stream>>>(r.f[x_].p, r.f[pd_].p, s, 9 * r.N);
+      ++r.c->launches;
+      COMBO_CK(cudaGetLastError());
+    }
+  };
   auto flush_x = [&]() {
     if (dfmg || it == 0) return;
-    ProfScope ps(c_, kTagCgUpdate, 216.0 * double(N_));
-    k_axpy<<<ew_grid(9 * N_), kEwThreads, 0, c_->stream>>>(x_, pd_, step_prev, 9 * N_);
-    ++c_->launches;
-    COMBO_CK(cudaGetLastError());
+    axpy_x(step_prev);
   };
+  auto cons = [&](size_t k) { return ConsCg{P(ap_, k), P(pd_, k), rk_[k].N}; };
   while (it < cfg_.cg_max) {
-    ConsCg cons{ap_, pd_, N_};
     count_ls();
     ++rep.ls_cg;
     if (dfmg) {
-      dfmg_matvec(c_, F_, shF_, r_, pd_, beta, it == 0, rb_);
+      dfmg_matvec(c_, P(F_, 0), shF_, P(r_, 0), P(pd_, 0), beta, it == 0, P(rb_, 0));
       ++c_->launches;
       COMBO_CK(cudaGetLastError());
-      project_fused(c_, cfg_.green, ProdLoad9{rb_, N_}, cons, 0, 20);
+      project_fused(c_, cfg_.green, ProdLoad9{P(rb_, 0), rk_[0].N}, cons(0), 20);
     } else {
-      // matvec fused into the Z-forward pass: r, F, cid, pdir (r/w), x (r/w,
-      // deferred update); composite packed tangents
-      ProdMatvec prod{{c_->mp, c_->cell_data(), F_, shF_, r_, pd_, beta, it == 0 ? 1 : 0, N_, x_, step_prev}};
-      const double mvb = (it == 0 ? 220.0 : 436.0) * double(N_) + 360.0 * double(c_->ncomp);
+      // r, F, cid, pdir (r/w), x (r/w, deferred update); composite packed tangents
+      auto mv = [&](size_t k) {
+        combo_ctx* m = rk_[k].c;
+        return ProdMatvec{{m->mp, m->cell_data(), P(F_, k), shF_, P(r_, k), P(pd_, k), beta, it == 0 ? 1 : 0,
+                           rk_[k].N, P(x_, k), step_prev}};
+      };
+      const double mvb = (it == 0 ? 220.0 : 436.0) * double(c_->N) + 360.0 * double(c_->ncomp);
       if (c_->plan->fuse_mv) {
-        project_fused(c_, cfg_.green, prod, cons, 0, 20, mvb);
+        project_group(c_, cfg_.green, mv, cons, 20, mvb);
       } else {
-        {
-          ProfScope ps(c_, kTagMatvec, mvb + 72.0 * double(N_));
-          k_matvec<<<g, kEwThreads, 0, c_->stream>>>(prod.a, rb_);
+        for (size_t k = 0; k < rk_.size(); ++k) {
+          combo_ctx* m = rk_[k].c;
+          ProfScope ps(m, kTagMatvec, mvb + 72.0 * double(rk_[k].N));
+          const MatvecArgs a = mv(k).a;
+          const int g = ew_grid(rk_[k].N);
+          if (m->plan->mvminb >= 4)
+            k_matvec<4><<<g, kEwThreads, 0, m->stream>>>(a, P(rb_, k));
+          else if (m->plan->mvminb == 3)
+            k_matvec<3><<<g, kEwThreads, 0, m->stream>>>(a, P(rb_, k));
+          else
+            k_matvec<><<<g, kEwThreads, 0, m->stream>>>(a, P(rb_, k));
+          ++m->launches;
+          COMBO_CK(cudaGetLastError());
         }
-        ++c_->launches;
-        COMBO_CK(cudaGetLastError());
-        project_fused(c_, cfg_.green, ProdLoad9{rb_, N_}, cons, 0, 20);
+        project_group(
+            c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; }, cons, 20);
       }
     }
     fetch_results(c_);
     const double pap = c_->hres[20];
     if (!(pap > 0.0)) {
       breakdown = true;
-      return it;  // this iteration's x update is not applied (solver.cpp:182-185)
+      // the previous iteration's x update was applied by this iteration's
+      // matvec; this iteration's is not applied (solver.cpp:182-185)
+      return it;
     }
     const double step = rr / pap;
-    if (dfmg) {
-      ProfScope ps(c_, kTagCgUpdate, 216.0 * double(N_));
-      k_axpy<<<ew_grid(9 * N_), kEwThreads, 0, c_->stream>>>(x_, pd_, step, 9 * N_);
-      ++c_->launches;
+    if (dfmg) axpy_x(step);
+    for (auto& r : rk_) {
+      double* part = part_ptr(r.c, nbc, 1);
+      ProfScope ps(r.c, kTagCgUpdate, 216.0 * double(r.N));
+      k_cg_update<<<unsigned(nbc), kEwThreads, 0, r.c->stream>>>(r.f[r_].p, r.f[ap_].p, step, r.N, chunks_of(r.c),
+                                                                   part);
+      ++r.c->launches;
+      COMBO_CK(cudaGetLastError());
     }
-    ensure_partials(c_, g);
-    {
-      ProfScope ps(c_, kTagCgUpdate, 216.0 * double(N_));
-      k_cg_update<<<g, kEwThreads, 0, c_->stream>>>(r_, ap_, step, 9 * N_, c_->partials.p);
-    }
-    ++c_->launches;
-    COMBO_CK(cudaGetLastError());
-    reduce_partials(c_, g, 1, 21);
+    group_reduce(c_, nbc, 1, 21);
     fetch_results(c_);
     ++it;
     step_prev = step;
@@ -992,12 +1147,12 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
       fetch_results(c_);
       rep.sweep = stats();
       if (rep.sweep.inadmissible_cells > 0) return false;
-      for (int q = 0; q < 9; ++q) pbar_[q] = c_->hres[q] / double(N_);
+      for (int q = 0; q < 9; ++q) pbar_[q] = c_->hres[q] / double(Ng_);
       count_ls();
       ++rep.ls_residual;
-      ProdLoad9 prod{rb_, N_};
-      ConsResid cons{r_, N_};
-      project_fused(c_, cfg_.green, prod, cons, 0, 9);
+      project_group(
+          c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
+          [&](size_t k) { return ConsResid{P(r_, k), rk_[k].N}; }, 9);
       fetch_results(c_);
       ss = c_->hres[9];
     } else {
@@ -1011,7 +1166,7 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
     rep.pbar_history.push_back({});
     std::memcpy(rep.pbar_history.back().data(), pbar_, sizeof pbar_);
     const double den = std::max(norm9(pbar_), stress_floor_);
-    const double resid = std::sqrt(ss / double(N_)) / den;
+    const double resid = std::sqrt(ss / double(Ng_)) / den;
     rep.residuals.push_back(resid);
     rep.outer_iters = it;
     if (cfg_.verbose) std::printf("  newton it %3d resid %.3e\n", it, resid);
@@ -1034,18 +1189,20 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
     combo_sweep_stats st_acc{};
     double ss_acc = 0.0;
     Shift9 sh_t{};
+    const int64_t nbc = chunk_blocks(c_);
     for (int ls = 0; ls < 10; ++ls) {
-      const int g = ew_grid(N_);
-      ensure_partials(c_, int64_t(g) * 9);
-      {
-        ProfScope ps(c_, kTagTrial, 216.0 * double(N_));
-        k_trial<<<g, kEwThreads, 0, c_->stream>>>(F_, shF_, x_, s, Fo_, N_, c_->partials.p);
+      for (size_t k = 0; k < rk_.size(); ++k) {
+        combo_ctx* m = rk_[k].c;
+        double* part = part_ptr(m, nbc, 9);
+        ProfScope ps(m, kTagTrial, 216.0 * double(rk_[k].N));
+        k_trial<<<unsigned(nbc), kEwThreads, 0, m->stream>>>(P(F_, k), shF_, P(x_, k), s, P(Fo_, k), rk_[k].N,
+                                                               chunks_of(m), part);
+        ++m->launches;
+        COMBO_CK(cudaGetLastError());
       }
-      ++c_->launches;
-      COMBO_CK(cudaGetLastError());
-      reduce_partials(c_, g, 9, 30);
+      group_reduce(c_, nbc, 9, 30);
       fetch_results(c_);
-      for (int q = 0; q < 9; ++q) sh_t.v[q] = fbar[q] - c_->hres[30 + q] / double(N_);
+      for (int q = 0; q < 9; ++q) sh_t.v[q] = fbar[q] - c_->hres[30 + q] / double(Ng_);
       reset_stats(c_);
       eval_sweep(Fo_, sh_t, 0.0, rb_, true, 0);
       last_eval_ = Fo_;
@@ -1054,16 +1211,16 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
       const combo_sweep_stats st = stats();
       if (st.inadmissible_cells == 0) {
         double pb[9];
-        for (int q = 0; q < 9; ++q) pb[q] = c_->hres[q] / double(N_);
+        for (int q = 0; q < 9; ++q) pb[q] = c_->hres[q] / double(Ng_);
         count_ls();
         ++rep.ls_trial;
-        ProdLoad9 prod{rb_, N_};
-        ConsResid cons{bn_, N_};
-        project_fused(c_, cfg_.green, prod, cons, 0, 9);
+        project_group(
+            c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
+            [&](size_t k) { return ConsResid{P(bn_, k), rk_[k].N}; }, 9);
         fetch_results(c_);
         const double ss_t = c_->hres[9];
         std::memcpy(pbar_, pb, sizeof pb);  // residual_from_stress sets pbar_ (:95)
-        const double rtrial = std::sqrt(ss_t / double(N_)) / std::max(norm9(pb), stress_floor_);
+        const double rtrial = std::sqrt(ss_t / double(Ng_)) / std::max(norm9(pb), stress_floor_);
         if (rtrial <= resid * (1.0 + 1e-12)) {
           accepted = true;
           st_acc = st;
@@ -1102,14 +1259,19 @@ void Solver::run(const double* fbar_target, combo_report& report) {
   {
     Shift9 one;
     for (int q = 0; q < 9; ++q) one.v[q] = I[q];
-    k_fill9<<<ew_grid(N_), kEwThreads, 0, c_->stream>>>(F_, one, N_);
-    ++c_->launches;
+    for (auto& r : rk_) {
+      k_fill9<<<ew_grid(r.N), kEwThreads, 0, r.c->stream>>>(r.f[F_].p, one, r.N);
+      ++r.c->launches;
+    }
   }
   shF_ = zero_shift();
   report.success = true;
-  DBuf<double> backup_f, backup_warm;
-  backup_f.alloc(size_t(9 * N_));
-  if (c_->ncomp) backup_warm.alloc(size_t(3 * c_->ncomp));
+  // per-rank backups of F and the warm starts (solver.cpp:313-315)
+  std::vector<DBuf<double>> backup_f(rk_.size()), backup_warm(rk_.size());
+  for (size_t k = 0; k < rk_.size(); ++k) {
+    backup_f[k].alloc(size_t(9 * rk_[k].N));
+    if (rk_[k].c->ncomp) backup_warm[k].alloc(size_t(3 * rk_[k].c->ncomp));
+  }
   DBuf<double> dfmg_backup;  // DfmgState warm starts (solver.cpp:315,330)
   if (cfg_.eval == COMBO_EVAL_DFMG) {
     // fresh DfmgState per solve (CellSolver ctor, solver.cpp:55)
@@ -1117,6 +1279,20 @@ void Solver::run(const double* fbar_target, combo_report& report) {
     COMBO_CK(cudaMemsetAsync(c_->dfmg_warm.p, 0, c_->dfmg_warm.n * 8, c_->stream));
     dfmg_backup.alloc(c_->dfmg_warm.n);
   }
+  auto save_or_restore = [&](bool save) {
+    for (size_t k = 0; k < rk_.size(); ++k) {
+      combo_ctx* m = rk_[k].c;
+      double* f = P(F_, k);
+      COMBO_CK(cudaMemcpyAsync(save ? backup_f[k].p : f, save ? f : backup_f[k].p,
+                               size_t(9 * rk_[k].N) * sizeof(double), cudaMemcpyDeviceToDevice, m->stream));
+      if (m->ncomp)
+        COMBO_CK(cudaMemcpyAsync(save ? backup_warm[k].p : m->warm.p, save ? m->warm.p : backup_warm[k].p,
+                                 size_t(3 * m->ncomp) * sizeof(double), cudaMemcpyDeviceToDevice, m->stream));
+    }
+    if (dfmg_backup.p)
+      COMBO_CK(cudaMemcpyAsync(save ? dfmg_backup.p : c_->dfmg_warm.p, save ? c_->dfmg_warm.p : dfmg_backup.p,
+                               dfmg_backup.n * sizeof(double), cudaMemcpyDeviceToDevice, c_->stream));
+  };
   try {
     while (t < 1.0 - 1e-12) {
       const double dt_try = std::min(dt, 1.0 - t);
@@ -1124,13 +1300,7 @@ void Solver::run(const double* fbar_target, combo_report& report) {
       for (int q = 0; q < 9; ++q) fbar[q] = I[q] + (t + dt_try) * h[q];
       // backup F (materialized) and warm starts
       materialize();
-      COMBO_CK(cudaMemcpyAsync(backup_f.p, F_, size_t(9 * N_) * sizeof(double), cudaMemcpyDeviceToDevice, c_->stream));
-      if (c_->ncomp)
-        COMBO_CK(cudaMemcpyAsync(backup_warm.p, c_->warm.p, size_t(3 * c_->ncomp) * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, c_->stream));
-      if (dfmg_backup.p)
-        COMBO_CK(cudaMemcpyAsync(dfmg_backup.p, c_->dfmg_warm.p, dfmg_backup.n * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, c_->stream));
+      save_or_restore(true);
       pin_mean(fbar);
       combo_host::StepRec rep;
       rep.t_start = t;
@@ -1146,15 +1316,9 @@ void Solver::run(const double* fbar_target, combo_report& report) {
         std::memcpy(fbar_prev, fbar, sizeof fbar);
         continue;
       }
-      COMBO_CK(cudaMemcpyAsync(F_, backup_f.p, size_t(9 * N_) * sizeof(double), cudaMemcpyDeviceToDevice, c_->stream));
+      save_or_restore(false);
       shF_ = zero_shift();
       pin_mean(fbar_prev);
-      if (c_->ncomp)
-        COMBO_CK(cudaMemcpyAsync(c_->warm.p, backup_warm.p, size_t(3 * c_->ncomp) * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, c_->stream));
-      if (dfmg_backup.p)
-        COMBO_CK(cudaMemcpyAsync(c_->dfmg_warm.p, dfmg_backup.p, dfmg_backup.n * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, c_->stream));
       ++report.bisections;
       if (report.bisections > cfg_.max_bisections) {
         report.steps.push_back(std::move(rep));
@@ -1174,11 +1338,17 @@ void Solver::run(const double* fbar_target, combo_report& report) {
   report.seconds_total = since(tic);
 }
 
-void Solver::final_stress(double* P) {
-  const double* fin = last_eval_ ? last_eval_ : F_;
-  const Shift9 sh = last_eval_ ? last_eval_shift_ : shF_;
+// P of the last evaluated state into out[k] (one pointer per rank)
+void Solver::final_stress(const std::vector<double*>& out) {
+  const int fin = last_eval_ >= 0 ? last_eval_ : F_;
+  const Shift9 sh = last_eval_ >= 0 ? last_eval_shift_ : shF_;
   reset_stats(c_);
-  eval_sweep(fin, sh, 0.0, P, false, 40);
+  if (cfg_.eval == COMBO_EVAL_DFMG) {
+    dfmg_sweep(c_, P(fin, 0), sh, 0.0, out[0], 40);
+    return;
+  }
+  for (size_t k = 0; k < rk_.size(); ++k) sweep_launch(rk_[k].c, P(fin, k), sh, 0.0, out[k], false);
+  group_reduce(c_, chunk_blocks(c_), 9, 40);
 }
 
 std::string report_json(const combo_report& r) {
@@ -1294,6 +1464,13 @@ int combo_ctx_destroy(combo_ctx* c) {
   if (!c) return COMBO_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& m : c->vm)
+    if (m->hres) cudaFreeHost(m->hres);
+  c->vm.clear();
+  try {
+    nccl_destroy(c);
+  } catch (...) {
+  }
   c->plan.reset();
   if (c->hres) cudaFreeHost(c->hres);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1356,14 +1533,84 @@ const char* combo_profile_json(combo_ctx* c) {
 }
 
 int combo_set_grid(combo_ctx* c, const int64_t dims[3], const double lengths[3]) {
-  return guarded(c, [&] { set_grid(c, dims, lengths); });
+  return guarded(c, [&] {
+    for (combo_ctx* m : members(c)) set_grid(m, dims, lengths);
+  });
+}
+
+// Slab decomposition along axis 0. Emulated: nranks ranks in
+// this process on this context's device (member contexts sharing its
+// stream; the transpose is a device copy) -- the decomposition-invariance
+// test harness. Must precede combo_bind_materials.
+int combo_ctx_set_virtual_ranks(combo_ctx* c, int nranks) {
+  return guarded(c, [&] {
+    if (nranks < 1) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "nranks must be >= 1");
+    if (c->nccl) throw ComboError(COMBO_ERR_STATE, "context already joined an NCCL decomposition");
+    COMBO_CK(cudaStreamSynchronize(c->stream));
+    c->vm.clear();
+    c->R = nranks;
+    c->q = 0;
+    c->bound = false;
+    for (int q = 1; q < nranks; ++q) {
+      auto m = std::make_unique<combo_ctx>();
+      m->device = c->device;
+      m->num_sms = c->num_sms;
+      m->stream = c->stream;
+      m->own_stream = false;
+      m->lead = c;
+      m->R = nranks;
+      m->q = q;
+      ensure_scratch(m.get());
+      c->vm.push_back(std::move(m));
+    }
+    if (c->has_grid) {
+      const auto d = c->dims;
+      const auto l = c->lengths;
+      for (combo_ctx* m : members(c)) set_grid(m, d.data(), l.data());
+    }
+  });
+}
+
+// One rank per process: this context is rank `rank` of `nranks`; nccl_id is
+// the 128-byte id from combo_nccl_unique_id on rank 0 (broadcast by the
+// caller, e.g. over torch.distributed). Must precede combo_bind_materials.
+int combo_ctx_set_ranks(combo_ctx* c, int nranks, int rank, const void* nccl_id) {
+  return guarded(c, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "bad rank / nranks");
+    if (!c->vm.empty()) throw ComboError(COMBO_ERR_STATE, "context hosts emulated ranks");
+    if (nranks > 1 && !nccl_id) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "nccl_id required for nranks > 1");
+    nccl_destroy(c);
+    c->R = nranks;
+    c->q = rank;
+    c->bound = false;
+    if (nranks > 1) nccl_init(c, nranks, rank, nccl_id);
+    if (c->has_grid) {
+      const auto d = c->dims;
+      const auto l = c->lengths;
+      set_grid(c, d.data(), l.data());
+    }
+  });
+}
+
+int combo_ctx_ranks(const combo_ctx* c, int* nranks, int* rank, int* local_ranks, int64_t* i0, int64_t* ni) {
+  if (!c) return COMBO_ERR_BAD_ARGUMENT;
+  if (nranks) *nranks = c->R;
+  if (rank) *rank = c->q;
+  if (local_ranks) *local_ranks = int(1 + c->vm.size());
+  const int64_t n = c->has_grid ? c->dims[0] / c->R : 0;
+  if (i0) *i0 = int64_t(c->q) * n;
+  if (ni) *ni = n;
+  return COMBO_OK;
 }
 
 // CellMaterials::CellMaterials (cell_material.cpp:12-55)
-int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengths[3], const uint8_t* kind,
+}  // extern "C"
+
+namespace {
+// binding of one slab: kind / c_plus / normal3 point at the slab's first cell
+static void bind_slab(combo_ctx* c, const int64_t dims[3], const double lengths[3], const uint8_t* kind,
                          const double* c_plus, const double* normal3, const combo_law* matrix,
                          const combo_law* inclusion, int combo, const combo_laminate_opts* lam, int mem) {
-  return guarded(c, [&] {
     if (!kind || !c_plus || !matrix || !inclusion) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
     set_grid(c, dims, lengths);
     const int64_t N = c->N;
@@ -1452,12 +1699,31 @@ int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengt
     c->mp.lam.back_projection = c->lam.back_projection;
     c->dfmg_warm.release();
     c->bound = true;
+}
+}  // namespace
+
+extern "C" {
+
+// the arrays describe the whole grid; every rank binds its slab of planes
+int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengths[3], const uint8_t* kind,
+                         const double* c_plus, const double* normal3, const combo_law* matrix,
+                         const combo_law* inclusion, int combo, const combo_laminate_opts* lam, int mem) {
+  return guarded(c, [&] {
+    if (!kind || !c_plus || !matrix || !inclusion) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
+    for (combo_ctx* m : members(c)) {
+      m->R = c->R;
+      set_grid(m, dims, lengths);
+      const int64_t off = int64_t(m->q) * m->N;
+      bind_slab(m, dims, lengths, kind + off, c_plus + off, normal3 ? normal3 + 3 * off : nullptr, matrix, inclusion,
+                combo, lam, mem);
+    }
   });
 }
 
 int combo_composite_cells(const combo_ctx* c, int64_t* count) {
   if (!c || !count) return COMBO_ERR_BAD_ARGUMENT;
-  *count = c->ncomp;
+  *count = c->ncomp;  // emulated ranks: all slabs; one rank per process: this slab
+  for (const auto& m : c->vm) *count += m->ncomp;
   return COMBO_OK;
 }
 
@@ -1477,6 +1743,7 @@ int combo_spectrum_bounds(combo_ctx* c, const double fbar[9], double* lo, double
 int combo_get_warm_starts(combo_ctx* c, double* warm3, int mem) {
   return guarded(c, [&] {
     require_bound(c);
+    require_single(c);
     const int64_t n = c->ncomp;
     if (!n) return;
     std::vector<double> soa(size_t(3 * n));
@@ -1494,6 +1761,7 @@ int combo_get_warm_starts(combo_ctx* c, double* warm3, int mem) {
 int combo_set_warm_starts(combo_ctx* c, const double* warm3, int mem) {
   return guarded(c, [&] {
     require_bound(c);
+    require_single(c);
     const int64_t n = c->ncomp;
     if (!n) return;
     std::vector<double> aos(size_t(3 * n));
@@ -1511,8 +1779,10 @@ int combo_set_warm_starts(combo_ctx* c, const double* warm3, int mem) {
 int combo_reset_warm_starts(combo_ctx* c) {
   return guarded(c, [&] {
     require_bound(c);
-    if (c->ncomp) COMBO_CK(cudaMemsetAsync(c->warm.p, 0, size_t(3 * c->ncomp) * 8, c->stream));
-    if (c->dfmg_warm.p) COMBO_CK(cudaMemsetAsync(c->dfmg_warm.p, 0, c->dfmg_warm.n * 8, c->stream));
+    for (combo_ctx* m : members(c)) {
+      if (m->ncomp) COMBO_CK(cudaMemsetAsync(m->warm.p, 0, size_t(3 * m->ncomp) * 8, m->stream));
+      if (m->dfmg_warm.p) COMBO_CK(cudaMemsetAsync(m->dfmg_warm.p, 0, m->dfmg_warm.n * 8, m->stream));
+    }
     COMBO_CK(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1526,6 +1796,7 @@ int combo_get_stream(combo_ctx* c, void** stream) {
 int combo_stress_sweep(combo_ctx* c, const double* F, double* P, combo_sweep_stats* st, int mem) {
   return guarded(c, [&] {
     require_bound(c);
+    require_single(c);
     ensure_scratch(c);
     const double* f = stage_in(c, F, mem, 0);
     double* p = stage_out(c, P, mem, 1);
@@ -1546,13 +1817,14 @@ int combo_stress_sweep(combo_ctx* c, const double* F, double* P, combo_sweep_sta
 int combo_tangent_matvec(combo_ctx* c, const double* F, const double* x, double* y, int mem) {
   return guarded(c, [&] {
     require_bound(c);
+    require_single(c);
     const double* f = stage_in(c, F, mem, 0);
     const double* xx = stage_in(c, x, mem, 1);
     double* yy = stage_out(c, y, mem, 2);
     c->scratch[3].alloc(size_t(9 * c->N));
     comp_tangents(c, f, zero_shift());
     MatvecArgs a{c->mp, c->cell_data(), f, zero_shift(), xx, c->scratch[3].p, 0.0, 1, c->N, nullptr, 0.0};
-    k_matvec<<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(a, yy);
+    k_matvec<><<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(a, yy);
     ++c->launches;
     COMBO_CK(cudaGetLastError());
     finish_out(c, y, yy, mem, size_t(9 * c->N));
@@ -1563,6 +1835,7 @@ int combo_tangent_matvec(combo_ctx* c, const double* F, const double* x, double*
 int combo_tangent45(combo_ctx* c, const double* F, double* t45, int mem) {
   return guarded(c, [&] {
     require_bound(c);
+    require_single(c);
     const double* f = stage_in(c, F, mem, 0);
     DBuf<double> t;
     double* dt = t45;
@@ -1602,16 +1875,31 @@ int combo_project(combo_ctx* c, int kind, const double* in, double* out, int mem
   return guarded(c, [&] {
     if (!c->has_grid) throw ComboError(COMBO_ERR_STATE, "no grid (combo_set_grid)");
     ensure_scratch(c);
-    const double* src = stage_in(c, in, mem, 0);
-    double* dst = stage_out(c, out, mem, 1);
-    project_fused(c, kind, ProdLoad9{src, c->N}, ConsStore9{dst, c->N}, 0, 0);
-    finish_out(c, out, dst, mem, size_t(9 * c->N));
+    // in / out: [9][N] of the grid (emulated ranks: split into / gathered
+    // from the slabs; one rank per process: this rank's slab)
+    const auto ms = members(c);
+    const int64_t Nl = c->N, Nt = Nl * int64_t(ms.size());
+    const auto h2d = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const auto d2h = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    for (size_t k = 0; k < ms.size(); ++k) {
+      ms[k]->scratch[0].alloc(size_t(9 * Nl));
+      ms[k]->scratch[1].alloc(size_t(9 * Nl));
+      COMBO_CK(cudaMemcpy2DAsync(ms[k]->scratch[0].p, size_t(Nl) * 8, in + int64_t(k) * Nl, size_t(Nt) * 8,
+                                 size_t(Nl) * 8, 9, h2d, c->stream));
+    }
+    project_group(
+        c, kind, [&](size_t k) { return ProdLoad9{ms[k]->scratch[0].p, Nl}; },
+        [&](size_t k) { return ConsStore9{ms[k]->scratch[1].p, Nl}; }, 0);
+    for (size_t k = 0; k < ms.size(); ++k)
+      COMBO_CK(cudaMemcpy2DAsync(out + int64_t(k) * Nl, size_t(Nt) * 8, ms[k]->scratch[1].p, size_t(Nl) * 8,
+                                 size_t(Nl) * 8, 9, d2h, c->stream));
     COMBO_CK(cudaStreamSynchronize(c->stream));
   });
 }
 
 int combo_fft_forward(combo_ctx* c, const int64_t dims[3], int ncomp, const double* in, double* out, int mem) {
   return guarded(c, [&] {
+    require_single(c);
     if (ncomp < 1 || ncomp > 9) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ncomp must be 1..9");
     double L[3] = {1, 1, 1};
     if (c->has_grid) std::memcpy(L, c->lengths.data(), sizeof L);
@@ -1631,7 +1919,7 @@ int combo_fft_forward(combo_ctx* c, const int64_t dims[3], int ncomp, const doub
     for (int64_t cc = 0; cc < ncomp; ++cc)
       for (int64_t i = 0; i < p.dims[0]; ++i)
         COMBO_CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(out) + size_t((cc * p.dims[0] + i) * p.dims[1] * p.n3c) * 16,
-                                   size_t(p.n3c) * 16, sv.spec + cc * sv.plane + i * sv.si, size_t(sv.sj) * 16,
+                                   size_t(p.n3c) * 16, sv.spec + cc * sv.cs + i * sv.si, size_t(sv.sj) * 16,
                                    size_t(p.n3c) * 16, size_t(p.dims[1]),
                                    mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                    c->stream));
@@ -1656,17 +1944,27 @@ int combo_solve(combo_ctx* c, const double fbar[9], const combo_solver_cfg* cfg,
     Solver s(c, *cfg);
     s.run(fbar, *rep);
     if (pbar) std::memcpy(pbar, s.pbar(), 9 * sizeof(double));
+    // outputs: [9][N] of the grid (emulated ranks gathered in slab order);
+    // with one rank per process, this rank's slab [9][N_local]
+    const auto ms = members(c);
+    auto gather = [&](double* out, std::vector<double*> src) {
+      const int64_t Nl = c->N, Nt = Nl * int64_t(ms.size());
+      const auto kind = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+      for (size_t k = 0; k < src.size(); ++k)
+        COMBO_CK(cudaMemcpy2DAsync(out + int64_t(k) * Nl, size_t(Nt) * 8, src[k], size_t(Nl) * 8, size_t(Nl) * 8, 9,
+                                   kind, c->stream));
+    };
     if (P_out) {
-      double* p = mem == COMBO_MEM_DEVICE ? P_out : s.bufs_[6].p;
+      std::vector<double*> p;
+      for (size_t k = 0; k < s.nranks(); ++k) p.push_back(s.scratch(k));
       s.final_stress(p);
-      finish_out(c, P_out, p, mem, size_t(9 * c->N));
+      gather(P_out, p);
     }
     if (F_out) {
       s.materialize();
-      if (mem == COMBO_MEM_DEVICE)
-        COMBO_CK(cudaMemcpyAsync(F_out, s.F(), size_t(9 * c->N) * 8, cudaMemcpyDeviceToDevice, c->stream));
-      else
-        COMBO_CK(cudaMemcpyAsync(F_out, s.F(), size_t(9 * c->N) * 8, cudaMemcpyDeviceToHost, c->stream));
+      std::vector<double*> f;
+      for (size_t k = 0; k < s.nranks(); ++k) f.push_back(s.F(k));
+      gather(F_out, f);
     }
     COMBO_CK(cudaStreamSynchronize(c->stream));
     rep->json = report_json(*rep);

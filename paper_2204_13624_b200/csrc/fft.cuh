@@ -262,18 +262,44 @@ __device__ void block_reduce_store(double (&acc)[NRED], double* partials, int64_
 }
 
 // ---------------------------------------------------------------- passes
-// Half spectrum: rows of n3p complex, row (c, i, j) at c plane + i si + j sj.
-// The engine stores j-major rows (si = n3p, sj = n1 n3p) so that the x lines
-// read by the three-channel X+Gamma pass are 4 KB apart (DRAM-page friendly)
-// and the one-channel Y pass takes the long stride with 128-byte segments.
+// Half spectrum: rows of n3p complex.
+//
+// Single slab (blocked = 0): row (c, i, j) at c cs + i si + j sj, with
+// i-major (si = n2 n3p, sj = n3p) or j-major (si = n3p, sj = n1 n3p) rows.
+//
+// Slab decomposition over R ranks (blocked = 1; ni = n1 / R planes per slab,
+// nj = n2 / R k2-columns per pencil): the slab side (z and y passes) keeps
+// planes [i0, i0 + ni) of every k2 and stores them blocked by destination
+// pencil s = j / nj:  A(c, il, j) = s blk + c cs + (il nj + j mod nj) n3p;
+// the pencil side (x pass + Gamma) keeps k2 in [j0, j0 + nj) of every plane,
+// blocked by source slab r = i / ni:  B(c, i, jl) = r blk + c cs +
+// ((i mod ni) nj + jl) n3p, with blk = 9 ni nj n3p and cs = ni nj n3p. Block s
+// of A on rank q is block q of B on rank s, so the transpose is one
+// all-to-all of equal contiguous blocks; with R = 1 both reduce to the
+// i-major single-slab layout.
 struct SpecView {
   double2* spec;
-  int64_t n1, n2, n3, n3c, n3p;
-  int64_t si, sj, plane;
-  // offset of the row of component c on z-line `line` = i n2 + j
+  int64_t n1, n2, n3, n3c, n3p;  // global grid, row length
+  int64_t cs;                    // component stride
+  int64_t si, sj;                // single-slab row strides
+  int64_t ni, nj, i0, j0, blk;   // slab / pencil extents and offsets
+  int blocked;
+  // slab side: local plane il, global k2 j
+  __host__ __device__ __forceinline__ int64_t rowA(int64_t il, int64_t j) const {
+    if (!blocked) return il * si + j * sj;
+    const int s = int(j) / int(nj);
+    return s * blk + (il * nj + (j - int64_t(s) * nj)) * n3p;
+  }
+  // pencil side: global plane i, local k2 jl
+  __host__ __device__ __forceinline__ int64_t rowB(int64_t i, int64_t jl) const {
+    if (!blocked) return i * si + jl * sj;
+    const int r = int(i) / int(ni);
+    return r * blk + ((i - int64_t(r) * ni) * nj + jl) * n3p;
+  }
+  // row of component c on local z-line `line` = il n2 + j
   __host__ __device__ __forceinline__ int64_t zrow(int64_t c, int64_t line) const {
-    const int64_t i = line / n2;
-    return c * plane + i * si + (line - i * n2) * sj;
+    const int64_t il = line / n2;
+    return c * cs + rowA(il, line - il * n2);
   }
 };
 
@@ -291,7 +317,7 @@ static __global__ void __launch_bounds__(kMaxFftThreads)
     zfwd_kernel(SpecView sv, Axis ax, int L, int ls, Prod prod, double* partials) {
   extern __shared__ double2 sm[];
   const int n = line_len<LOG2N>(ax);
-  const int64_t nlines_tot = sv.n1 * sv.n2;
+  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int64_t line0 = int64_t(blockIdx.x) * L;
   const int nlines = int(min(int64_t(L), nlines_tot - line0));
   const int nreal = 9 * nlines;
@@ -341,7 +367,7 @@ static __global__ void __launch_bounds__(kMaxFftThreads)
     zinv_kernel(SpecView sv, Axis ax, int L, int ls, double scale, Cons cons, double* partials) {
   extern __shared__ double2 sm[];
   const int n = line_len<LOG2N>(ax);
-  const int64_t nlines_tot = sv.n1 * sv.n2;
+  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int64_t line0 = int64_t(blockIdx.x) * L;
   const int nlines = int(min(int64_t(L), nlines_tot - line0));
   const int nreal = 9 * nlines;
@@ -395,16 +421,16 @@ static __global__ void __launch_bounds__(kMaxFftThreads) ypass_kernel(SpecView s
   const int n2 = line_len<LOG2N>(ax);
   const int c = blockIdx.z, i = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
-  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(i) * sv.si + kc0;
+  double2* base = sv.spec + int64_t(c) * sv.cs + kc0;
   for (int t = threadIdx.x; t < n2 * W; t += blockDim.x) {
     const int j = t / W, col = t - j * W;
-    if (col < w) sm[t] = base[int64_t(j) * sv.sj + col];
+    if (col < w) sm[t] = base[sv.rowA(i, j) + col];
   }
   __syncthreads();
   fft_lines<LOG2N, INV, true>(sm, ax, W, W, 1);
   for (int t = threadIdx.x; t < n2 * W; t += blockDim.x) {
     const int j = t / W, col = t - j * W;
-    if (col < w) base[int64_t(j) * sv.sj + col] = sm[t];
+    if (col < w) base[sv.rowA(i, j) + col] = sm[t];
   }
 }
 
@@ -470,11 +496,11 @@ static __global__ void __launch_bounds__(kMaxFftThreads) xgamma_kernel(SpecView 
   const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
   const int W3 = 3 * W;
-  const int64_t plane = sv.plane;  // component stride
-  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.sj + kc0;
+  const int64_t plane = sv.cs;  // component stride
+  double2* base = sv.spec + int64_t(3 * rg) * plane + kc0;  // pencil side, local k2 j
   for (int t = threadIdx.x; t < n1 * W3; t += blockDim.x) {
     const int i = t / W3, rem = t - i * W3, cc = rem / W, col = rem - cc * W;
-    if (col < w) sm[t] = base[int64_t(cc) * plane + int64_t(i) * sv.si + col];
+    if (col < w) sm[t] = base[int64_t(cc) * plane + sv.rowB(i, j) + col];
   }
   __syncthreads();
   fft_lines<LOG2N, false, true>(sm, ax, W3, W3, 1);
@@ -484,7 +510,7 @@ static __global__ void __launch_bounds__(kMaxFftThreads) xgamma_kernel(SpecView 
       double2 v[3];
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc) v[cc] = sm[k1 * W3 + cc * W + col];
-      gamma_row(G, rg, k1, j, kc0 + col, sv.n1, sv.n2, sv.n3, v);
+      gamma_row(G, rg, k1, sv.j0 + j, kc0 + col, sv.n1, sv.n2, sv.n3, v);
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc) sm[k1 * W3 + cc * W + col] = v[cc];
     }
@@ -493,7 +519,7 @@ static __global__ void __launch_bounds__(kMaxFftThreads) xgamma_kernel(SpecView 
   fft_lines<LOG2N, true, true>(sm, ax, W3, W3, 1);
   for (int t = threadIdx.x; t < n1 * W3; t += blockDim.x) {
     const int i = t / W3, rem = t - i * W3, cc = rem / W, col = rem - cc * W;
-    if (col < w) base[int64_t(cc) * plane + int64_t(i) * sv.si + col] = sm[t];
+    if (col < w) base[int64_t(cc) * plane + sv.rowB(i, j) + col] = sm[t];
   }
 }
 
@@ -504,16 +530,16 @@ static __global__ void __launch_bounds__(kMaxFftThreads) xpass_kernel(SpecView s
   const int n1 = line_len<LOG2N>(ax);
   const int c = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
-  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(j) * sv.sj + kc0;
+  double2* base = sv.spec + int64_t(c) * sv.cs + kc0;
   for (int t = threadIdx.x; t < n1 * W; t += blockDim.x) {
     const int i = t / W, col = t - i * W;
-    if (col < w) sm[t] = base[int64_t(i) * sv.si + col];
+    if (col < w) sm[t] = base[sv.rowB(i, j) + col];
   }
   __syncthreads();
   fft_lines<LOG2N, INV, true>(sm, ax, W, W, 1);
   for (int t = threadIdx.x; t < n1 * W; t += blockDim.x) {
     const int i = t / W, col = t - i * W;
-    if (col < w) base[int64_t(i) * sv.si + col] = sm[t];
+    if (col < w) base[sv.rowB(i, j) + col] = sm[t];
   }
 }
 

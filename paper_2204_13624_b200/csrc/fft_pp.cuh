@@ -37,7 +37,7 @@ static __global__ void __launch_bounds__(512, 1) ypass_pp(SpecView sv, const dou
     const int64_t rest = tile / ntk;
     const int64_t i = rest % sv.n1, c = rest / sv.n1;
     w = min(W, int(sv.n3c) - kt * W);
-    return sv.spec + c * sv.plane + i * sv.si + int64_t(kt) * W;
+    return sv.spec + c * sv.cs + i * sv.si + int64_t(kt) * W;
   };
   auto prefetch = [&](double2* buf, int64_t tile) {
     int w;
@@ -88,7 +88,7 @@ static __global__ void __launch_bounds__(256, 1) xgamma_pp(SpecView sv, const do
   extern __shared__ double2 sm[];
   const int ntk = int((sv.n3c + W - 1) / W);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
-  const int64_t plane = sv.plane;
+  const int64_t plane = sv.cs;  // single slab only (pipelines are off when blocked)
   const int64_t rowstride = sv.si;
   const int chs = (N + N / 8) * W;
   auto base_of = [&](int64_t tile, int& w, int64_t& j, int& rg, int& kc0) {
@@ -169,7 +169,7 @@ static __global__ void __launch_bounds__(384, 2)
   constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
   constexpr int LSD = (LS + 1) & ~1;  // even double stride: 16-byte aligned rows
   extern __shared__ double2 sm[];
-  const int64_t nlines_tot = sv.n1 * sv.n2;
+  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int u = threadIdx.x % TL, p = threadIdx.x / TL;
   const int rla = 2 * p, rlb = 2 * p + 1;
   const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
@@ -255,7 +255,7 @@ static __global__ void __launch_bounds__(384, 2) zinv_pp(SpecView sv, const doub
                                                          double* partials) {
   constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
   extern __shared__ double2 sm[];
-  const int64_t nlines_tot = sv.n1 * sv.n2;
+  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int nc = int(sv.n3c);
   const int u = threadIdx.x % TL, p = threadIdx.x / TL;
   const int rla = 2 * p, rlb = 2 * p + 1;

@@ -218,7 +218,7 @@ static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
     zfwd_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, Prod prod, double* partials) {
   constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
   extern __shared__ double2 sm[];
-  const int64_t nlines_tot = sv.n1 * sv.n2;
+  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
   const int nlines = int(min(int64_t(nl_per_block), nlines_tot - line0));
   const int nreal = 9 * nlines;
@@ -293,7 +293,7 @@ static __global__ void __launch_bounds__(512, 2)
             double* partials) {
   constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
   extern __shared__ double2 sm[];
-  const int64_t nlines_tot = sv.n1 * sv.n2;
+  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
   const int nlines = int(min(int64_t(nl_per_block), nlines_tot - line0));
   const int nreal = 9 * nlines;
@@ -364,17 +364,17 @@ static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(i) * sv.si + kc0 + line;
+  double2* base = sv.spec + int64_t(c) * sv.cs + kc0 + line;
   double2 v[1][8];
   if (active) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[0][q] = base[int64_t(rr_first_pos<L, false>(u, q)) * sv.sj];
+    for (int q = 0; q < 8; ++q) v[0][q] = base[sv.rowA(i, rr_first_pos<L, false>(u, q))];
   }
   auto addr = [&](int, int pos) { return pad8(pos) * W + line; };
   rr_stages<L, INV, false, 0, 1>(v, u, active, sm, tw, addr);
   if (active) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) base[int64_t(rr_final_pos<L, false>(u, q)) * sv.sj] = v[0][q];
+    for (int q = 0; q < 8; ++q) base[sv.rowA(i, rr_final_pos<L, false>(u, q))] = v[0][q];
   }
 }
 
@@ -391,14 +391,14 @@ static __global__ void __launch_bounds__(256, 2) ypass_rr2(SpecView sv, const do
   const int line = threadIdx.x % W2, u = threadIdx.x / W2;
   const bool active = u < N / 8;
   const bool on[2] = {line < w, line + W2 < w};
-  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(i) * sv.si + kc0 + line;
+  double2* base = sv.spec + int64_t(c) * sv.cs + kc0 + line;
   double2 v[2][8];
   if (active) {
 #pragma unroll
     for (int ch = 0; ch < 2; ++ch)
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        v[ch][q] = on[ch] ? base[int64_t(rr_first_pos<L, false>(u, q)) * sv.sj + ch * W2] : make_double2(0.0, 0.0);
+        v[ch][q] = on[ch] ? base[sv.rowA(i, rr_first_pos<L, false>(u, q)) + ch * W2] : make_double2(0.0, 0.0);
   }
   auto addr = [&](int ch, int pos) { return pad8(pos) * W + ch * W2 + line; };
   rr_stages<L, INV, false, 0, 2>(v, u, active, sm, tw, addr);
@@ -407,7 +407,7 @@ static __global__ void __launch_bounds__(256, 2) ypass_rr2(SpecView sv, const do
     for (int ch = 0; ch < 2; ++ch)
       if (on[ch]) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) base[int64_t(rr_final_pos<L, false>(u, q)) * sv.sj + ch * W2] = v[ch][q];
+        for (int q = 0; q < 8; ++q) base[sv.rowA(i, rr_final_pos<L, false>(u, q)) + ch * W2] = v[ch][q];
       }
   }
 }
@@ -423,15 +423,14 @@ static __global__ void __launch_bounds__(256, 2)
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  const int64_t plane = sv.plane;
-  const int64_t rowstride = sv.si;
-  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.sj + kc0 + line;
+  const int64_t plane = sv.cs;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + kc0 + line;  // pencil side, local k2 j
   double2 v[3][8];
   if (active) {
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[ch][q] = base[int64_t(ch) * plane + rr_first_pos<L, false>(u, q) * rowstride];
+      for (int q = 0; q < 8; ++q) v[ch][q] = base[int64_t(ch) * plane + sv.rowB(rr_first_pos<L, false>(u, q), j)];
   }
   const int chs = (N + N / 8) * W;  // channel stride in smem
   auto addr = [&](int ch, int pos) { return ch * chs + pad8(pos) * W + line; };
@@ -442,7 +441,7 @@ static __global__ void __launch_bounds__(256, 2)
     for (int q = 0; q < 8; ++q) {
       const int64_t k1 = rr_final_pos<L, false>(u, q);
       double2 t[3] = {v[0][q], v[1][q], v[2][q]};
-      gamma_row(G, rg, k1, j, k3, sv.n1, sv.n2, sv.n3, t);
+      gamma_row(G, rg, k1, sv.j0 + j, k3, sv.n1, sv.n2, sv.n3, t);
       v[0][q] = t[0];
       v[1][q] = t[1];
       v[2][q] = t[2];
@@ -454,7 +453,7 @@ static __global__ void __launch_bounds__(256, 2)
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) base[int64_t(ch) * plane + rr_final_pos<L, true>(u, q) * rowstride] = v[ch][q];
+      for (int q = 0; q < 8; ++q) base[int64_t(ch) * plane + sv.rowB(rr_final_pos<L, true>(u, q), j)] = v[ch][q];
   }
 }
 
@@ -559,21 +558,20 @@ static __global__ void __launch_bounds__(MAXT, MINB)
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  const int64_t plane = sv.plane;
-  const int64_t rowstride = sv.si;
-  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.sj + kc0 + line;
+  const int64_t plane = sv.cs;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + kc0 + line;  // pencil side, local k2 j
   double2 v[3][8];
   if (active) {
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[ch][q] = base[int64_t(ch) * plane + rr_first_pos<L, false>(u, q) * rowstride];
+      for (int q = 0; q < 8; ++q) v[ch][q] = base[int64_t(ch) * plane + sv.rowB(rr_first_pos<L, false>(u, q), j)];
   }
   const int chs = (N + N / 8) * W;
   auto addr = [&](int ch, int pos) { return ch * chs + pad8(pos) * W + line; };
   rr_stages<L, false, false, 0, 3>(v, u, active, sm, tw, addr);
   if (active) {
-    const GammaCol col = gamma_col(G, j, kc0 + line, sv.n2, sv.n3);
+    const GammaCol col = gamma_col(G, sv.j0 + j, kc0 + line, sv.n2, sv.n3);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       double2 t[3] = {v[0][q], v[1][q], v[2][q]};
@@ -588,7 +586,7 @@ static __global__ void __launch_bounds__(MAXT, MINB)
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) base[int64_t(ch) * plane + rr_final_pos<L, true>(u, q) * rowstride] = v[ch][q];
+      for (int q = 0; q < 8; ++q) base[int64_t(ch) * plane + sv.rowB(rr_final_pos<L, true>(u, q), j)] = v[ch][q];
   }
 }
 
@@ -695,16 +693,15 @@ static __global__ void __launch_bounds__(MAXT, MINB)
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  const int64_t plane = sv.plane;
-  const int64_t rowstride = sv.si;
-  double2* base = sv.spec + int64_t(3 * rg) * plane + int64_t(j) * sv.sj + kc0 + line;
-  const RankCol<KIND> col = rank_col<KIND>(G, rg, j, kc0 + line, sv.n2, sv.n3);
+  const int64_t plane = sv.cs;
+  double2* base = sv.spec + int64_t(3 * rg) * plane + kc0 + line;  // pencil side, local k2 j
+  const RankCol<KIND> col = rank_col<KIND>(G, rg, sv.j0 + j, kc0 + line, sv.n2, sv.n3);
   double2 v[2][8];
   if (active) {
     double2 t1[8], t2[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int64_t o = int64_t(rr_first_pos<L, false>(u, q)) * rowstride;
+      const int64_t o = sv.rowB(rr_first_pos<L, false>(u, q), j);
       v[0][q] = base[o];
       t1[q] = base[plane + o];
       t2[q] = base[2 * plane + o];
@@ -726,7 +723,7 @@ static __global__ void __launch_bounds__(MAXT, MINB)
   if (active) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int64_t o = int64_t(rr_final_pos<L, true>(u, q)) * rowstride;
+      const int64_t o = sv.rowB(rr_final_pos<L, true>(u, q), j);
       base[o] = v[0][q];
       base[plane + o] = cmul(col.o1, v[1][q]);
       base[2 * plane + o] = cmul(col.o2, v[1][q]);
@@ -743,18 +740,17 @@ static __global__ void __launch_bounds__(512, 2) xpass_rr(SpecView sv, const dou
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
-  const int64_t rowstride = sv.si;
-  double2* base = sv.spec + int64_t(c) * sv.plane + int64_t(j) * sv.sj + kc0 + line;
+  double2* base = sv.spec + int64_t(c) * sv.cs + kc0 + line;
   double2 v[1][8];
   if (active) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[0][q] = base[rr_first_pos<L, false>(u, q) * rowstride];
+    for (int q = 0; q < 8; ++q) v[0][q] = base[sv.rowB(rr_first_pos<L, false>(u, q), j)];
   }
   auto addr = [&](int, int pos) { return pad8(pos) * W + line; };
   rr_stages<L, INV, false, 0, 1>(v, u, active, sm, tw, addr);
   if (active) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) base[rr_final_pos<L, false>(u, q) * rowstride] = v[0][q];
+    for (int q = 0; q < 8; ++q) base[sv.rowB(rr_final_pos<L, false>(u, q), j)] = v[0][q];
   }
 }
 

@@ -94,17 +94,38 @@ struct Shift9 {
   double v[9];
 };
 
+// Deterministic, decomposition-invariant reductions: block b of a chunked
+// launch owns cells [p plane + k C, min(p plane + (k + 1) C, (p + 1) plane))
+// of local plane p = b / cpp (k = b mod cpp, C = kChunk). Chunks never
+// straddle a plane, so a slab of whole planes owns a contiguous range of the
+// global chunk list and the fixed-order combination of all chunk partials is
+// the same for any number of slabs (reference: deterministic chunk-4096
+// reductions, parallel.hpp:40-104).
+constexpr int kChunk = 2048;
+struct Chunks {
+  int64_t plane;  // cells per plane (n2 n3)
+  int cpp;        // chunks per plane
+};
+__device__ __forceinline__ void chunk_range(const Chunks& k, int64_t& beg, int64_t& end) {
+  const int64_t p = blockIdx.x / k.cpp;
+  const int64_t j = blockIdx.x - p * k.cpp;
+  beg = p * k.plane + j * kChunk;
+  end = min(beg + kChunk, (p + 1) * k.plane);
+}
+
 // out = P(F_in + shift) - alpha (F_in + shift); partial sums of P (P-bar).
 static __global__ void __launch_bounds__(kEwThreads) k_sweep(MatParams M, CellData cd, const double* __restrict__ fin,
                                                       Shift9 sh, double alpha, double* __restrict__ out,
-                                                      int64_t N, int writeback, Stats* st, double* partials) {
+                                                      int64_t N, Chunks ch, int writeback, Stats* st,
+                                                      double* partials) {
   double acc[9];
 #pragma unroll
   for (int c = 0; c < 9; ++c) acc[c] = 0.0;
   unsigned long long inad = 0, fail = 0, bp = 0;
   unsigned int itmax = 0;
-  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
-       cell += int64_t(gridDim.x) * blockDim.x) {
+  int64_t beg, end;
+  chunk_range(ch, beg, end);
+  for (int64_t cell = beg + threadIdx.x; cell < end; cell += blockDim.x) {
     double f[9], p[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell] + sh.v[c];
@@ -178,7 +199,8 @@ __device__ __forceinline__ void mv_cell(const MatvecArgs& a, int64_t cell, doubl
   }
 }
 
-static __global__ void __launch_bounds__(kEwThreads) k_matvec(MatvecArgs a, double* __restrict__ q) {
+template <int MINB = 1>
+static __global__ void __launch_bounds__(kEwThreads, MINB) k_matvec(MatvecArgs a, double* __restrict__ q) {
   for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < a.N;
        cell += int64_t(gridDim.x) * blockDim.x) {
     double y[9];
@@ -214,12 +236,18 @@ static __global__ void __launch_bounds__(128) k_comp_tangent(MatParams M, CellDa
 // CG step P6 (solver.cpp:187-190): r -= step * ap ; partial sum of r^2
 static __global__ void __launch_bounds__(kEwThreads) k_cg_update(double* __restrict__ r,
                                                           const double* __restrict__ ap, double step,
-                                                          int64_t n, double* partials) {
+                                                          int64_t N, Chunks ch, double* partials) {
   double acc[1] = {0.0};
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const double rv = r[i] + (-step) * ap[i];
-    r[i] = rv;
-    acc[0] += rv * rv;
+  int64_t beg, end;
+  chunk_range(ch, beg, end);
+  for (int64_t cell = beg + threadIdx.x; cell < end; cell += blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      const int64_t i = c * N + cell;
+      const double rv = r[i] + (-step) * ap[i];
+      r[i] = rv;
+      acc[0] += rv * rv;
+    }
   }
   block_reduce_store<1>(acc, partials, blockIdx.x);
 }
@@ -233,12 +261,14 @@ static __global__ void k_axpy(double* __restrict__ x, const double* __restrict__
 // ftrial = (F + shiftF) + s x ; per-component sums for pin_mean
 static __global__ void __launch_bounds__(kEwThreads) k_trial(const double* __restrict__ f, Shift9 sh,
                                                       const double* __restrict__ x, double s,
-                                                      double* __restrict__ ft, int64_t N, double* partials) {
+                                                      double* __restrict__ ft, int64_t N, Chunks ch,
+                                                      double* partials) {
   double acc[9];
 #pragma unroll
   for (int c = 0; c < 9; ++c) acc[c] = 0.0;
-  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
-       cell += int64_t(gridDim.x) * blockDim.x) {
+  int64_t beg, end;
+  chunk_range(ch, beg, end);
+  for (int64_t cell = beg + threadIdx.x; cell < end; cell += blockDim.x) {
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
       const double v = (f[c * N + cell] + sh.v[c]) + s * x[c * N + cell];
@@ -251,12 +281,13 @@ static __global__ void __launch_bounds__(kEwThreads) k_trial(const double* __res
 
 // f = f + shift (materialize), per-component sums of the result
 static __global__ void __launch_bounds__(kEwThreads) k_materialize(double* __restrict__ f, Shift9 sh, int64_t N,
-                                                            double* partials) {
+                                                            Chunks ch, double* partials) {
   double acc[9];
 #pragma unroll
   for (int c = 0; c < 9; ++c) acc[c] = 0.0;
-  for (int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; cell < N;
-       cell += int64_t(gridDim.x) * blockDim.x) {
+  int64_t beg, end;
+  chunk_range(ch, beg, end);
+  for (int64_t cell = beg + threadIdx.x; cell < end; cell += blockDim.x) {
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
       const double v = f[c * N + cell] + sh.v[c];
