@@ -183,6 +183,15 @@ int combo_ctx_set_virtual_ranks(combo_ctx* ctx, int nranks);
 int combo_ctx_set_ranks(combo_ctx* ctx, int nranks, int rank, const void* nccl_id128);
 int combo_ctx_ranks(const combo_ctx* ctx, int* nranks, int* rank, int* local_ranks, int64_t* i0,
                     int64_t* ni);
+/* Layout introspection (host only): spectrum row offset (complex units) of
+ * (c, i, j) on the slab side (side 0: i local plane, j global column) or the
+ * pencil side (side 1: i global plane, j local column) of rank `rank`; cell
+ * range [beg, end) of reduction chunk `block` of a slab of `nplanes` planes
+ * (chunks never straddle planes, so partials are rank-count invariant). */
+int combo_slab_row(const int64_t dims[3], int nranks, int rank, int side, int64_t c, int64_t i, int64_t j,
+                   int64_t* off);
+int combo_chunk_range(const int64_t dims[3], int64_t nplanes, int64_t block, int64_t* beg, int64_t* end,
+                      int64_t* nblocks);
 
 /* ------------------------------------------------------------------ binding */
 /* SimGrid (field.hpp:16-28) for operator calls that need no materials

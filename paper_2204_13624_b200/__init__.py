@@ -21,4 +21,6 @@ from .combo import (  # noqa: F401
     load_library,
     GREEN,
     SCHEME,
+    slab_row,
+    chunk_range,
 )

@@ -96,6 +96,8 @@ SIGNATURES = {
     "combo_ctx_set_virtual_ranks": (C.c_int, [_VP, C.c_int]),
     "combo_ctx_set_ranks": (C.c_int, [_VP, C.c_int, C.c_int, _VP]),
     "combo_ctx_ranks": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    "combo_slab_row": (C.c_int, [_I64, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, _VP]),
+    "combo_chunk_range": (C.c_int, [_I64, C.c_int64, C.c_int64, _VP, _VP, _VP]),
     "combo_bind_materials": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, C.POINTER(Law), C.POINTER(Law), C.c_int,
                                        C.POINTER(LamOpts), C.c_int]),
     "combo_composite_cells": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
@@ -227,6 +229,27 @@ def _i64(x):
 
 def _f64(x):
     return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+def slab_row(dims, nranks, rank, side, c, i, j):
+    """Spectrum row offset (complex units) of (c, i, j) in the slab-side
+    (side 0) or pencil-side (side 1) buffer of `rank` (combo_slab_row)."""
+    off = C.c_int64()
+    rc = load_library().combo_slab_row(_i64(dims), int(nranks), int(rank), int(side), int(c), int(i), int(j),
+                                       C.byref(off))
+    if rc:
+        raise ComboError(rc, "combo_slab_row")
+    return off.value
+
+
+def chunk_range(dims, nplanes, block):
+    """(beg, end, nblocks) of reduction chunk `block` of a slab of `nplanes`
+    planes (combo_chunk_range)."""
+    b, e, n = C.c_int64(), C.c_int64(), C.c_int64()
+    rc = load_library().combo_chunk_range(_i64(dims), int(nplanes), int(block), C.byref(b), C.byref(e), C.byref(n))
+    if rc:
+        raise ComboError(rc, "combo_chunk_range")
+    return b.value, e.value, n.value
 
 
 class Context:

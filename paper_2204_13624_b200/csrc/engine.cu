@@ -1592,6 +1592,47 @@ int combo_ctx_set_ranks(combo_ctx* c, int nranks, int rank, const void* nccl_id)
   });
 }
 
+// Host-side layout introspection (no device work): the spectrum row offset
+// of (component c, plane i, column j) on the slab side (side 0: i local to
+// the rank's slab, j global) or the pencil side (side 1: i global, j local),
+// and the cell range of chunk `block` of a slab of `nplanes` planes. Used by
+// the multi-process CPU tests to drive the same layout through gloo.
+int combo_slab_row(const int64_t dims[3], int nranks, int rank, int side, int64_t c, int64_t i, int64_t j,
+                   int64_t* off) {
+  if (!dims || !off || nranks < 1 || rank < 0 || rank >= nranks || dims[0] % nranks || dims[1] % nranks)
+    return COMBO_ERR_BAD_ARGUMENT;
+  SpecView v{};
+  v.n1 = dims[0];
+  v.n2 = dims[1];
+  v.n3 = dims[2];
+  v.n3c = dims[2] / 2 + 1;
+  v.n3p = (v.n3c + 7) / 8 * 8;
+  v.blocked = nranks > 1;
+  v.ni = dims[0] / nranks;
+  v.nj = dims[1] / nranks;
+  v.i0 = rank * v.ni;
+  v.j0 = rank * v.nj;
+  v.blk = 9 * v.ni * v.nj * v.n3p;
+  v.cs = nranks > 1 ? v.ni * v.nj * v.n3p : v.n1 * v.n2 * v.n3p;
+  v.si = v.n2 * v.n3p;
+  v.sj = v.n3p;
+  *off = c * v.cs + (side == 0 ? v.rowA(i, j) : v.rowB(i, j));
+  return COMBO_OK;
+}
+
+int combo_chunk_range(const int64_t dims[3], int64_t nplanes, int64_t block, int64_t* beg, int64_t* end,
+                      int64_t* nblocks) {
+  if (!dims || nplanes < 1) return COMBO_ERR_BAD_ARGUMENT;
+  const int64_t plane = dims[1] * dims[2];
+  const int64_t cpp = (plane + kChunk - 1) / kChunk;
+  if (nblocks) *nblocks = nplanes * cpp;
+  if (block < 0 || block >= nplanes * cpp) return COMBO_ERR_BAD_ARGUMENT;
+  const int64_t p = block / cpp, k = block - p * cpp;
+  if (beg) *beg = p * plane + k * kChunk;
+  if (end) *end = std::min(p * plane + (k + 1) * kChunk, (p + 1) * plane);
+  return COMBO_OK;
+}
+
 int combo_ctx_ranks(const combo_ctx* c, int* nranks, int* rank, int* local_ranks, int64_t* i0, int64_t* ni) {
   if (!c) return COMBO_ERR_BAD_ARGUMENT;
   if (nranks) *nranks = c->R;
