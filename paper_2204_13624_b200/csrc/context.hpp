@@ -110,7 +110,8 @@ struct FftPlan {
   int xv = 4;  // X+Gamma kernel variant (2 = xgamma_rr, 3 = xgamma_v3, 4 = rank-1 xgamma_v4)
   int xminb = 2;  // xgamma_v4 blocks per SM (launch bound)
   int yminb = 2;  // y pass blocks per SM (launch bound)
-  int mvminb = 1;  // CG matvec blocks per SM (launch bound)
+  bool split_sweep = true;  // composite Newton pass + pure streaming pass (COMBO_SPLIT_SWEEP=0: one pass)
+  bool mv_bulk = true;  // bulk-staged CG matvec (COMBO_MV_BULK=0: one cell per thread, direct loads)
   bool y2 = false;  // y pass with two columns per thread (ypass_rr2)
   bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
@@ -223,6 +224,9 @@ struct combo_ctx {
   combo_host::DBuf<combo_dev::Stats> dstats;
   double* hres = nullptr;              // pinned mirror of dres + stats
   combo_host::DBuf<double> scratch[4];  // operator-level staging (9N each)
+  // solver field slots (9N each), kept resident across solve() calls so a
+  // solve does not pay cudaMalloc/cudaFree of ~8 fields (77 GB at 512^3)
+  combo_host::DBuf<double> solver_fields[8];
 
   // CUDA-event profiling of every kernel launch (combo_profile_*)
   struct ProfRec {

@@ -200,7 +200,9 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->pipe_y = knob("COMBO_PIPE_Y", 0) != 0;
   p->pipe_x = knob("COMBO_PIPE_X", 0) != 0;
   p->xv = knob("COMBO_XV", 4);
-  p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;  // fused: 24.7 ms vs 15.5 + 5.7 split (512^3)
+  p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
+  p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
+  p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;  // fused: 24.7 ms vs 15.5 + 5.7 split (512^3)
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
   if (n3 >= 8) {
     const int64_t tl = n3 / 8;
@@ -437,6 +439,41 @@ bool pp_axis(int64_t n) {
   for (int l = 3; l <= 10; ++l)
     if (n == (int64_t(1) << l)) return true;
   return false;
+}
+
+// CG matvec: bulk-staged persistent kernel (one CTA per SM) when the rows
+// are 16-byte aligned, else one cell per thread with direct loads.
+template <bool FIRST, bool HASX>
+void launch_matvec_bulk(combo_ctx* c, const MatvecArgs& a, double* q) {
+  using S = combo_dev::MvStage<FIRST, HASX>;
+  constexpr int kMaxSmem = 227 * 1024;
+  const int stages = std::min(4, (kMaxSmem - 128) / S::kBytes);
+  const size_t smem = 128 + size_t(stages) * S::kBytes;
+  auto kern = combo_dev::k_matvec_bulk<FIRST, HASX>;
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    COMBO_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  const int64_t tiles = std::max<int64_t>(1, a.N / combo_dev::kMvT);
+  const int grid = int(std::min<int64_t>(tiles, c->num_sms));
+  kern<<<grid, combo_dev::kMvT + 32, smem, c->stream>>>(a, q, stages);
+}
+
+void launch_matvec(combo_ctx* c, const MatvecArgs& a, double* q) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool bulk = c->plan && c->plan->mv_bulk && a.N % 2 == 0 && al16(a.r) && al16(a.fin) && al16(a.pdir) &&
+                    (a.xv == nullptr || al16(a.xv)) && al16(a.cd.cid);
+  if (!bulk) {
+    combo_dev::k_matvec<><<<ew_grid(a.N), kEwThreads, 0, c->stream>>>(a, q);
+    return;
+  }
+  if (a.first)
+    launch_matvec_bulk<true, false>(c, a, q);
+  else if (a.xv)
+    launch_matvec_bulk<false, true>(c, a, q);
+  else
+    launch_matvec_bulk<false, false>(c, a, q);
 }
 
 template <class Prod>
@@ -685,8 +722,20 @@ void sweep_launch(combo_ctx* c, const double* fin, const Shift9& sh, double alph
   double* part = part_ptr(c, nb, 9);
   // F read + out write + cid, composite meta (n, c+, c-) and warm r/w
   ProfScope ps(c, kTagSweep, 148.0 * double(c->N) + 88.0 * double(c->ncomp));
-  k_sweep<<<unsigned(nb), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, alpha, out, c->N, chunks_of(c),
-                                                      writeback ? 1 : 0, stats_ptr(c), part);
+  if (c->plan && c->plan->split_sweep && fin != out) {  // pass 1 writes out before pass 2 reads fin
+    if (c->ncomp > 0) {
+      const unsigned g = unsigned(std::min<int64_t>((c->ncomp + 127) / 128, int64_t(c->num_sms) * 64));
+      k_sweep_comp<<<g, 128, 0, c->stream>>>(
+          c->mp, c->cell_data(), fin, sh, out, c->N, writeback ? 1 : 0, stats_ptr(c));
+      ++c->launches;
+      COMBO_CK(cudaGetLastError());
+    }
+    k_sweep_pure<<<unsigned(nb), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, alpha, out, c->N,
+                                                             chunks_of(c), stats_ptr(c), part);
+  } else {
+    k_sweep<<<unsigned(nb), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, alpha, out, c->N,
+                                                        chunks_of(c), writeback ? 1 : 0, stats_ptr(c), part);
+  }
   ++c->launches;
   COMBO_CK(cudaGetLastError());
 }
@@ -871,7 +920,7 @@ struct LsBudget {};
 struct SolverRank {
   combo_ctx* c;
   int64_t N;
-  DBuf<double> f[8];
+  DBuf<double>* f;  // c->solver_fields
 };
 
 // The solver runs every rank hosted by the leader context in lockstep: each
@@ -887,7 +936,8 @@ class Solver {
       SolverRank& r = rk_.back();
       r.c = m;
       r.N = m->N;
-      for (auto& b : r.f) b.alloc(size_t(9 * r.N));
+      r.f = m->solver_fields;
+      for (int q = 0; q < 8; ++q) r.f[q].alloc(size_t(9 * r.N));
     }
     if (rk_.size() > 1 || c->R > 1) {
       if (cfg.eval == COMBO_EVAL_DFMG)
@@ -1083,13 +1133,7 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
           combo_ctx* m = rk_[k].c;
           ProfScope ps(m, kTagMatvec, mvb + 72.0 * double(rk_[k].N));
           const MatvecArgs a = mv(k).a;
-          const int g = ew_grid(rk_[k].N);
-          if (m->plan->mvminb >= 4)
-            k_matvec<4><<<g, kEwThreads, 0, m->stream>>>(a, P(rb_, k));
-          else if (m->plan->mvminb == 3)
-            k_matvec<3><<<g, kEwThreads, 0, m->stream>>>(a, P(rb_, k));
-          else
-            k_matvec<><<<g, kEwThreads, 0, m->stream>>>(a, P(rb_, k));
+          launch_matvec(m, a, P(rb_, k));
           ++m->launches;
           COMBO_CK(cudaGetLastError());
         }
@@ -1865,7 +1909,7 @@ int combo_tangent_matvec(combo_ctx* c, const double* F, const double* x, double*
     c->scratch[3].alloc(size_t(9 * c->N));
     comp_tangents(c, f, zero_shift());
     MatvecArgs a{c->mp, c->cell_data(), f, zero_shift(), xx, c->scratch[3].p, 0.0, 1, c->N, nullptr, 0.0};
-    k_matvec<><<<ew_grid(c->N), kEwThreads, 0, c->stream>>>(a, yy);
+    launch_matvec(c, a, yy);
     ++c->launches;
     COMBO_CK(cudaGetLastError());
     finish_out(c, y, yy, mem, size_t(9 * c->N));

@@ -16,6 +16,7 @@
 #include "fft.cuh"
 #include "fft_rr.cuh"
 #include "material.cuh"
+#include "stage.cuh"
 
 namespace combo_dev {
 
@@ -140,6 +141,68 @@ static __global__ void __launch_bounds__(kEwThreads) k_sweep(MatParams M, CellDa
   block_reduce_store<9>(acc, partials, blockIdx.x);
 }
 
+// Split sweep, pass 1: the laminate Newton of every composite cell
+// (finite_strain_solve, cell_material.cpp:139-145), one composite per
+// thread over the compact composite list, so the per-cell Newton no longer
+// serialises the pure cells of mixed warps. Writes the raw P of each
+// composite cell (0 when inadmissible) into out; pass 2 folds it in.
+static __global__ void __launch_bounds__(128) k_sweep_comp(MatParams M, CellData cd, const double* __restrict__ fin,
+                                                           Shift9 sh, double* __restrict__ out, int64_t N,
+                                                           int writeback, Stats* st) {
+  unsigned long long inad = 0, fail = 0, bp = 0;
+  unsigned int itmax = 0;
+  for (int64_t id = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; id < cd.ncomp;
+       id += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t cell = cd.ccell[id];
+    double f[9], p[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell] + sh.v[c];
+    if (!cell_stress(M, cd, cell, f, p, writeback != 0, fail, bp, itmax)) ++inad;
+#pragma unroll
+    for (int c = 0; c < 9; ++c) out[c * N + cell] = p[c];
+  }
+  warp_stats(st, inad, fail, bp, itmax);
+}
+
+// Split sweep, pass 2: NH stress of the pure cells, composite P read back
+// from pass 1; out = P - alpha F; chunk partial sums of P in the same order
+// as k_sweep (bitwise the same results).
+static __global__ void __launch_bounds__(kEwThreads) k_sweep_pure(MatParams M, CellData cd,
+                                                                  const double* __restrict__ fin, Shift9 sh,
+                                                                  double alpha, double* __restrict__ out, int64_t N,
+                                                                  Chunks ch, Stats* st, double* partials) {
+  double acc[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) acc[c] = 0.0;
+  unsigned long long inad = 0;
+  int64_t beg, end;
+  chunk_range(ch, beg, end);
+  for (int64_t cell = beg + threadIdx.x; cell < end; cell += blockDim.x) {
+    const int32_t id = cd.cid[cell];
+    double f[9], p[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell] + sh.v[c];
+    if (id >= 0) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) p[c] = out[c * N + cell];
+    } else {
+      NhState s;
+      if (!law_eval(id == -2 ? M.law[1] : M.law[0], f, p, s)) {
+#pragma unroll
+        for (int c = 0; c < 9; ++c) p[c] = 0.0;
+        ++inad;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      acc[c] += p[c];
+      out[c * N + cell] = alpha != 0.0 ? p[c] + (-alpha) * f[c] : p[c];
+    }
+  }
+  warp_stats(st, inad, 0, 0, 0);
+  block_reduce_store<9>(acc, partials, blockIdx.x);
+}
+
 // CG step P1 (solver.cpp:186-197, deferred): x += step_prev * pdir_old (the
 // x update of the previous iteration, applied where pdir_old is read anyway),
 // pdir = first ? r : r + beta * pdir_old ; y = A(F) : pdir (matrix free NH,
@@ -207,6 +270,111 @@ static __global__ void __launch_bounds__(kEwThreads, MINB) k_matvec(MatvecArgs a
     mv_cell(a, cell, y);
 #pragma unroll
     for (int c = 0; c < 9; ++c) q[c * a.N + cell] = y[c];
+  }
+}
+
+// Bulk-staged matvec (same arithmetic as k_matvec, bitwise): a producer warp
+// streams the tile's component rows (r, F, pdir, x: 9 rows of kMvT cells
+// each, plus the cell ids) into a ring of shared-memory stages with
+// cp.async.bulk; 8 consumer warps compute one cell per thread from shared
+// memory and store pdir, x and q. Cells past the last full tile are done by
+// block 0 with direct loads. Requires N even and 16-byte aligned rows.
+constexpr int kMvT = 256;
+
+template <bool FIRST, bool HASX>
+struct MvStage {
+  static constexpr int kRows = 18 + (FIRST ? 0 : 9) + ((!FIRST && HASX) ? 9 : 0);
+  static constexpr int kBytes = kRows * kMvT * 8 + kMvT * 4;
+};
+
+template <bool FIRST, bool HASX>
+static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs a, double* __restrict__ q,
+                                                                      int nstages) {
+  using S = MvStage<FIRST, HASX>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + 8;
+  unsigned char* buf = smem_raw + 128;
+  const int64_t N = a.N;
+  const int64_t nfull = N / kMvT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kMvT / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kMvT / 32) {  // producer
+    if (lane == 0) {
+      Ring rg(nstages);
+      int k = 0;
+      for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x, ++k, rg.next()) {
+        if (k >= nstages) mbar_wait(&empty[rg.s], rg.phase ^ 1u);
+        double* d = reinterpret_cast<double*>(buf + size_t(rg.s) * S::kBytes);
+        const int64_t off = t * kMvT;
+        constexpr uint32_t rb = kMvT * 8;
+        mbar_expect_tx(&full[rg.s], S::kBytes);
+#pragma unroll 1
+        for (int c = 0; c < 9; ++c) {
+          bulk_g2s(d + c * kMvT, a.r + c * N + off, rb, &full[rg.s]);
+          bulk_g2s(d + (9 + c) * kMvT, a.fin + c * N + off, rb, &full[rg.s]);
+          if (!FIRST) bulk_g2s(d + (18 + c) * kMvT, a.pdir + c * N + off, rb, &full[rg.s]);
+          if (!FIRST && HASX) bulk_g2s(d + (27 + c) * kMvT, a.xv + c * N + off, rb, &full[rg.s]);
+        }
+        bulk_g2s(d + S::kRows * kMvT, a.cd.cid + off, kMvT * 4, &full[rg.s]);
+      }
+    }
+    return;
+  }
+  const int tid = threadIdx.x;
+  Ring rg(nstages);
+  for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x, rg.next()) {
+    mbar_wait(&full[rg.s], rg.phase);
+    const double* d = reinterpret_cast<const double*>(buf + size_t(rg.s) * S::kBytes);
+    const int64_t cell = t * kMvT + tid;
+    double x[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) x[c] = d[c * kMvT + tid];
+    if (!FIRST) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        const double po = d[(18 + c) * kMvT + tid];
+        if (HASX) a.xv[c * N + cell] = d[(27 + c) * kMvT + tid] + a.step_prev * po;
+        x[c] += a.beta * po;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) a.pdir[c * N + cell] = x[c];
+    const int32_t id = reinterpret_cast<const int32_t*>(d + S::kRows * kMvT)[tid];
+    double y[9];
+    if (id >= 0) {
+      packed45_apply(a.cd.t45 + id, a.cd.ncomp, x, y);
+    } else {
+      double f[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) f[c] = d[(9 + c) * kMvT + tid] + a.sh.v[c];
+      const LawP L = id == -2 ? a.M.law[1] : a.M.law[0];
+      NhState s;
+      if (law_state(L, f, s))
+        law_apply(L, s, x, y);
+      else
+#pragma unroll
+        for (int c = 0; c < 9; ++c) y[c] = x[c];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[rg.s]);
+#pragma unroll
+    for (int c = 0; c < 9; ++c) q[c * N + cell] = y[c];
+  }
+  if (blockIdx.x == 0) {
+    for (int64_t cell = nfull * kMvT + tid; cell < N; cell += kMvT) {
+      double y[9];
+      mv_cell(a, cell, y);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) q[c * N + cell] = y[c];
+    }
   }
 }
 

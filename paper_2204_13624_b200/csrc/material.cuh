@@ -158,6 +158,16 @@ __device__ inline bool law_eval(const LawP& L, const double* f, double* p, NhSta
   }
   return true;
 }
+// The tangent state only (G, ln J) of law_eval: bitwise the same state
+// without forming P (the CG matvec needs A, not P).
+__device__ inline bool law_state(const LawP& L, const double* f, NhState& s) {
+  if (L.kind != 0) return true;
+  const double j = det3(f);
+  if (!(j > 0.0)) return false;
+  inv_transpose(f, s.g);
+  s.lnj = log(j);
+  return true;
+}
 __device__ inline void law_apply(const LawP& L, const NhState& s, const double* x, double* y) {
   if (L.kind == 0) {
     nh_apply(L, s, x, y);
