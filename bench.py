@@ -296,7 +296,10 @@ def main():
         kind_h.copy_(kind.cpu())
         cp_h.copy_(cp.cpu())
         nrm_h.copy_(nrm.reshape(-1).cpu())
-        f_h = torch.empty(9 * N_local, dtype=torch.float64, pin_memory=True)  # this rank's slab
+        # SolveResult{f, p, pbar} (solver.hpp:57-62): both fields come back to
+        # pinned host buffers of this rank's slab
+        f_h = torch.empty(9 * N_local, dtype=torch.float64, pin_memory=True)
+        p_h = torch.empty(9 * N_local, dtype=torch.float64, pin_memory=True)
         e_ms = []
         ls_e = 0
         for _ in range(max(1, args.steps)):
@@ -305,7 +308,7 @@ def main():
             t0 = time.perf_counter()
             cm2 = CellMaterials(ctx, dims, kind_h, cp_h, nrm_h, neo_hookean(*cfg.matrix),
                                 neo_hookean(*cfg.inclusion))
-            r2 = cm2.solve(fbar, f_out=f_h, **kw)
+            r2 = cm2.solve(fbar, f_out=f_h, p_out=p_h, **kw)
             ctx.synchronize()
             e_ms.append((time.perf_counter() - t0) * 1000.0)
             ls_e += r2["report"]["ls_total"]
@@ -315,7 +318,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_tot = float(t.item())
         e2e = {"value": N * ls_e / (e_tot / 1000.0), "unit": "boxel-iterations/s",
-               "h2d_bytes_per_step": N_local * (1 + 8 + 24), "d2h_bytes_per_step": 9 * N_local * 8 + 72,
+               "h2d_bytes_per_step": N_local * (1 + 8 + 24), "d2h_bytes_per_step": 2 * 9 * N_local * 8 + 72,
                "ms_per_step": e_tot / len(e_ms)}
         cm = CellMaterials(ctx, dims, kind, cp, nrm, neo_hookean(*cfg.matrix), neo_hookean(*cfg.inclusion))
 

@@ -292,4 +292,7 @@ struct ProfScope {
   ProfScope(combo_ctx* ctx, int tag, double bytes);
   ~ProfScope();
 };
+// device-side CellMaterials binding of one slab (bind.cu)
+void bind_cells_device(combo_ctx* c, const uint8_t* kind, const double* cp, const double* n3, int combo,
+                       double c_min);
 }  // namespace combo_host

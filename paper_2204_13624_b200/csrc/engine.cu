@@ -224,7 +224,8 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     const int64_t ls = n3 + n3 / 8, lsd = (ls + 1) & ~int64_t(1);
     p->pzbuf = int(std::max({np * ls, (9 * Lz * lsd + 1) / 2, 9 * Lz * p->n3p}));
   }
-  p->swap = knob("COMBO_SWAP", 0) != 0;  // j-major rows: x 5.5 ms, y 4.7 ms; i-major: x 6.3, y 4.2 (512^3)
+  // j-major rows (single slab): x+Gamma 5.9 ms, y 4.05 / 4.09 ms; i-major: 6.8, 4.01 / 4.03 (512^3, round 1)
+  p->swap = knob("COMBO_SWAP", 1) != 0;
   if (d[1] >= 8) {
     int Wy = int(std::min<int64_t>(8, p->n3c));
     // i-major rows: 256-thread tiles measured faster than 512 at n2 = 512
@@ -1699,72 +1700,29 @@ static void bind_slab(combo_ctx* c, const int64_t dims[3], const double lengths[
     if (!kind || !c_plus || !matrix || !inclusion) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
     set_grid(c, dims, lengths);
     const int64_t N = c->N;
-    std::vector<uint8_t> hk(static_cast<size_t>(N));
-    std::vector<double> hc(static_cast<size_t>(N)), hn;
-    if (mem == COMBO_MEM_DEVICE) {
-      COMBO_CK(cudaMemcpy(hk.data(), kind, size_t(N), cudaMemcpyDeviceToHost));
-      COMBO_CK(cudaMemcpy(hc.data(), c_plus, size_t(N) * 8, cudaMemcpyDeviceToHost));
-    } else {
-      std::memcpy(hk.data(), kind, size_t(N));
-      std::memcpy(hc.data(), c_plus, size_t(N) * 8);
-    }
-    const double* nptr = normal3;
-    if (normal3 && mem == COMBO_MEM_DEVICE) {
-      hn.resize(size_t(3 * N));
-      COMBO_CK(cudaMemcpy(hn.data(), normal3, size_t(3 * N) * 8, cudaMemcpyDeviceToHost));
-      nptr = hn.data();
-    }
     combo_laminate_opts opts{0.0, 1e-10, 0.0, 50, 1, 0.0};
     if (lam) opts = *lam;
-    std::vector<int32_t> cid(static_cast<size_t>(N));
-    std::vector<double> nx, ny, nz, cp, cm;
-    std::vector<int64_t> ccell;
-    for (int64_t i = 0; i < N; ++i) {
-      const size_t si = size_t(i);
-      if (hk[si] == 0) {
-        cid[si] = -1;
-      } else if (hk[si] == 1) {
-        cid[si] = -2;
-      } else {
-        const double cpl = hc[si];
-        if (combo && cpl >= opts.c_min && 1.0 - cpl >= opts.c_min) {
-          // ComboMeta::make (laminate.cpp:28-34)
-          if (!(cpl > 0.0) || !(cpl < 1.0))
-            throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ComboMeta: volume fraction must lie in (0,1)");
-          if (!nptr) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ComboMeta: zero normal");
-          const double a = nptr[3 * si], b = nptr[3 * si + 1], d = nptr[3 * si + 2];
-          const double len = std::sqrt(a * a + b * b + d * d);
-          if (!(len > 0.0)) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "ComboMeta: zero normal");
-          cid[si] = int32_t(nx.size());
-          ccell.push_back(i);
-          nx.push_back(a / len);
-          ny.push_back(b / len);
-          nz.push_back(d / len);
-          cp.push_back(cpl);
-          cm.push_back(1.0 - cpl);
-        } else {
-          cid[si] = cpl >= 0.5 ? -2 : -1;
-        }
+    // the grid arrays go to the device once (host callers) and the cell
+    // binding runs there (bind.cu)
+    DBuf<uint8_t> dk;
+    DBuf<double> dc, dn;
+    const uint8_t* kd = kind;
+    const double* cd = c_plus;
+    const double* nd = normal3;
+    if (mem != COMBO_MEM_DEVICE) {
+      dk.alloc(size_t(N));
+      dc.alloc(size_t(N));
+      COMBO_CK(cudaMemcpyAsync(dk.p, kind, size_t(N), cudaMemcpyHostToDevice, c->stream));
+      COMBO_CK(cudaMemcpyAsync(dc.p, c_plus, size_t(N) * 8, cudaMemcpyHostToDevice, c->stream));
+      kd = dk.p;
+      cd = dc.p;
+      if (normal3) {
+        dn.alloc(size_t(3 * N));
+        COMBO_CK(cudaMemcpyAsync(dn.p, normal3, size_t(3 * N) * 8, cudaMemcpyHostToDevice, c->stream));
+        nd = dn.p;
       }
     }
-    c->ncomp = int64_t(nx.size());
-    c->cid.alloc(size_t(N));
-    COMBO_CK(cudaMemcpy(c->cid.p, cid.data(), size_t(N) * 4, cudaMemcpyHostToDevice));
-    const size_t nc = size_t(std::max<int64_t>(c->ncomp, 1));
-    c->nrm.alloc(3 * nc);
-    c->cp.alloc(nc);
-    c->cm.alloc(nc);
-    c->warm.alloc(3 * nc);
-    if (c->ncomp) {
-      COMBO_CK(cudaMemcpy(c->nrm.p, nx.data(), nx.size() * 8, cudaMemcpyHostToDevice));
-      COMBO_CK(cudaMemcpy(c->nrm.p + c->ncomp, ny.data(), ny.size() * 8, cudaMemcpyHostToDevice));
-      COMBO_CK(cudaMemcpy(c->nrm.p + 2 * c->ncomp, nz.data(), nz.size() * 8, cudaMemcpyHostToDevice));
-      COMBO_CK(cudaMemcpy(c->cp.p, cp.data(), cp.size() * 8, cudaMemcpyHostToDevice));
-      COMBO_CK(cudaMemcpy(c->cm.p, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice));
-    }
-    COMBO_CK(cudaMemset(c->warm.p, 0, 3 * nc * 8));
-    c->ccell.alloc(nc);
-    if (c->ncomp) COMBO_CK(cudaMemcpy(c->ccell.p, ccell.data(), ccell.size() * 8, cudaMemcpyHostToDevice));
+    bind_cells_device(c, kd, cd, nd, combo, opts.c_min);
     c->t45.release();
     c->law_m = *matrix;
     c->law_i = *inclusion;
