@@ -110,6 +110,10 @@ struct FftPlan {
   int xv = 4;  // X+Gamma kernel variant (2 = xgamma_rr, 3 = xgamma_v3, 4 = rank-1 xgamma_v4)
   int xminb = 2;  // xgamma_v4 blocks per SM (launch bound)
   int yminb = 2;  // y pass blocks per SM (launch bound)
+  bool fuse_zy = false;  // plane-pipelined Z/Y passes through L2 (COMBO_FUSE_ZY=0: five separate passes)
+  bool fuse_discard = true;
+  int fuse_wy = 0;  // y columns per fused tile (0: fill the z tile's threads)  // COMBO_FUSE_DISCARD=0: keep the consumed rows (write-back)
+  combo_host::DBuf<unsigned> sched;  // ticket + per-plane counters of the fused passes
   bool split_sweep = true;  // composite Newton pass + pure streaming pass (COMBO_SPLIT_SWEEP=0: one pass)
   bool mv_bulk = true;  // bulk-staged CG matvec (COMBO_MV_BULK=0: one cell per thread, direct loads)
   bool y2 = false;  // y pass with two columns per thread (ypass_rr2)

@@ -15,6 +15,7 @@
 
 #include "context.hpp"
 #include "fft_pp.cuh"
+#include "fft_fused.cuh"
 
 using namespace combo_dev;
 
@@ -202,7 +203,10 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->xv = knob("COMBO_XV", 4);
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
-  p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;  // fused: 24.7 ms vs 15.5 + 5.7 split (512^3)
+  p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
+  p->fuse_zy = knob("COMBO_FUSE_ZY", 0) != 0;  // experimental: see fft_fused.cuh
+  p->fuse_discard = knob("COMBO_FUSE_DISCARD", 1) != 0;
+  p->fuse_wy = knob("COMBO_FUSE_WY", 0);  // fused: 24.7 ms vs 15.5 + 5.7 split (512^3)
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
   if (n3 >= 8) {
     const int64_t tl = n3 / 8;
@@ -682,6 +686,99 @@ void launch_x_plain(combo_ctx* c) {
   ++c->launches;
   COMBO_CK(cudaGetLastError());
 }
+// ---- plane-pipelined Z/Y passes (fft_fused.cuh)
+bool fuse_zy_ok(const combo_ctx* c) {
+  const FftPlan& p = *c->plan;
+#ifndef COMBO_WITH_FUSED_ZY
+  return false;
+#endif
+  return p.fuse_zy && !p.pipe_z && !p.pipe_y && pp_axis(p.dims[1]) && pp_axis(p.dims[2]) && p.rzL > 0;
+}
+
+struct FusedGeom {
+  int threads, wy;
+  size_t smem;
+};
+FusedGeom fused_geom(const FftPlan& p) {
+  const int tly = int(p.dims[1] / 8);
+  FusedGeom g;
+  g.wy = std::max(1, std::min<int>(8, p.rzT / tly));
+  if (p.fuse_wy > 0) g.wy = p.fuse_wy;
+  g.wy = int(std::min<int64_t>(g.wy, p.n3c));
+  g.threads = std::max(p.rzT, (g.wy * tly + 31) / 32 * 32);
+  g.smem = std::max(p.rzsmem, size_t((p.dims[1] + p.dims[1] / 8) * g.wy) * sizeof(double2));
+  return g;
+}
+
+combo_dev::PlaneSched plane_sched(combo_ctx* c, const FusedGeom& g) {
+  FftPlan& p = *c->plan;
+  p.sched.alloc(size_t(1 + p.ni));
+  COMBO_CK(cudaMemsetAsync(p.sched.p, 0, (1 + p.ni) * sizeof(unsigned), c->stream));
+  combo_dev::PlaneSched s;
+  s.ticket = p.sched.p;
+  s.done = p.sched.p + 1;
+  s.nplanes = p.ni;
+  s.zl = p.rzL;
+  s.nz = int(p.dims[1] / p.rzL);
+  s.wy = g.wy;
+  s.nyk = int((p.n3c + g.wy - 1) / g.wy);
+  s.discard = p.fuse_discard ? 1 : 0;
+  return s;
+}
+
+#ifdef COMBO_WITH_FUSED_ZY  // experimental, off by default (ptxas time; see fft_fused.cuh)
+template <class Prod>
+void launch_zy_fwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
+  FftPlan& p = *c->plan;
+  ProfScope ps(c, kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
+  const FusedGeom g = fused_geom(p);
+  const combo_dev::PlaneSched s = plane_sched(c, g);
+  dispatch_log2(p.dims[2], [&](auto Lz) {
+    constexpr int LZ = decltype(Lz)::value;
+    dispatch_log2(p.dims[1], [&](auto Ly) {
+      constexpr int LY = decltype(Ly)::value;
+      if constexpr (LZ >= 3 && LY >= 3) {
+        auto k = zy_fwd_fused<Prod, LZ, LY>;
+        smem_attr(k, g.smem);
+        const int64_t items = p.ni * (s.nz + 9 * s.nyk);
+        const int grid = pp_grid(c, k, g.threads, g.smem, items);
+        k<<<unsigned(grid), g.threads, g.smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.ax[1].tw.p, prod, s);
+      }
+    });
+  });
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+}
+
+template <class Cons>
+int64_t launch_yz_inv(combo_ctx* c, const Cons& cons) {
+  FftPlan& p = *c->plan;
+  ProfScope ps(c, kTagZinv, spec_bytes(c) + 72.0 * double(c->N) * Cons::FIELDS);
+  const FusedGeom g = fused_geom(p);
+  const combo_dev::PlaneSched s = plane_sched(c, g);
+  const int64_t nb = p.ni * s.nz;  // z tiles = partial slots, as launch_zinv
+  double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
+  const double scale = 1.0 / double(c->Ng);
+  dispatch_log2(p.dims[2], [&](auto Lz) {
+    constexpr int LZ = decltype(Lz)::value;
+    dispatch_log2(p.dims[1], [&](auto Ly) {
+      constexpr int LY = decltype(Ly)::value;
+      if constexpr (LZ >= 3 && LY >= 3) {
+        auto k = yz_inv_fused<Cons, LZ, LY>;
+        smem_attr(k, g.smem);
+        const int64_t items = p.ni * (s.nz + 9 * s.nyk);
+        const int grid = pp_grid(c, k, g.threads, g.smem, items);
+        k<<<unsigned(grid), g.threads, g.smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.ax[1].tw.p, scale, cons, part,
+                                                            s);
+      }
+    });
+  });
+  ++c->launches;
+  COMBO_CK(cudaGetLastError());
+  return nb;
+}
+#endif
+
 // Projection Pi(tau) = alpha Gamma^0 tau (green.cpp:133-151) with fused
 // producer / consumer, over every rank hosted by the leader c: prodf(k) /
 // consf(k) build member k's producer and consumer. z and y passes run on
@@ -694,14 +791,33 @@ void project_group(combo_ctx* c, int kind, PF&& prodf, CF&& consf, int slot_cons
   using Prod = std::decay_t<decltype(prodf(size_t(0)))>;
   using Cons = std::decay_t<decltype(consf(size_t(0)))>;
   static_assert(Prod::NRED == 0, "producer reductions are not combined across ranks");
-  for (size_t k = 0; k < ms.size(); ++k) launch_zfwd(ms[k], prodf(k), prod_bytes);
-  for (auto* m : ms) launch_y<false>(m);
+  const bool fz = !Prod::CELL && fuse_zy_ok(c);
+  for (size_t k = 0; k < ms.size(); ++k) {
+#ifdef COMBO_WITH_FUSED_ZY
+    if (fz) {
+      launch_zy_fwd(ms[k], prodf(k), prod_bytes);
+      continue;
+    }
+#endif
+    launch_zfwd(ms[k], prodf(k), prod_bytes);
+  }
+  if (!fz)
+    for (auto* m : ms) launch_y<false>(m);
   exchange(c, true);
   for (auto* m : ms) launch_xgamma(m, kind);
   exchange(c, false);
-  for (auto* m : ms) launch_y<true>(m);
+  if (!fz)
+    for (auto* m : ms) launch_y<true>(m);
   int64_t nbc = 0;
-  for (size_t k = 0; k < ms.size(); ++k) nbc = launch_zinv(ms[k], consf(k));
+  for (size_t k = 0; k < ms.size(); ++k) {
+#ifdef COMBO_WITH_FUSED_ZY
+    if (fz) {
+      nbc = launch_yz_inv(ms[k], consf(k));
+      continue;
+    }
+#endif
+    nbc = launch_zinv(ms[k], consf(k));
+  }
   if (Cons::NRED) group_reduce(c, nbc, Cons::NRED, slot_cons);
 }
 

@@ -213,14 +213,12 @@ __device__ void group_reduce_store(double (&sc)[NSC > 0 ? NSC : 1], double pa, d
 constexpr int kMaxZRows = 1024;  // 9 x lines per block (T <= 512 bounds it)
 // Pairs of real lines (comp c of z-line l, enumerated rl = 9 l + c) are packed
 // as one complex line; T = npair * N/8 threads, thread -> (pair, u).
+// one tile: z-lines [line0, line0 + nlines) of the slab
 template <class Prod, int L>
-static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
-    zfwd_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, Prod prod, double* partials) {
+__device__ __forceinline__ void zfwd_tile(const SpecView& sv, const double2* __restrict__ tw, int64_t line0,
+                                          int nlines, const Prod& prod) {
   constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
   extern __shared__ double2 sm[];
-  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
-  const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
-  const int nlines = int(min(int64_t(nl_per_block), nlines_tot - line0));
   const int nreal = 9 * nlines;
   const int npair = (nreal + 1) >> 1;
   const int u = threadIdx.x % TL, p = threadIdx.x / TL;
@@ -287,40 +285,83 @@ static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
   }
 }
 
-template <class Cons, int L>
-static __global__ void __launch_bounds__(512, 2)
-    zinv_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, double scale, Cons cons,
-            double* partials) {
-  constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
-  extern __shared__ double2 sm[];
+template <class Prod, int L>
+static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
+    zfwd_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, Prod prod, double*) {
   const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
-  const int nlines = int(min(int64_t(nl_per_block), nlines_tot - line0));
+  zfwd_tile<Prod, L>(sv, tw, line0, int(min(int64_t(nl_per_block), nlines_tot - line0)), prod);
+}
+
+// one tile: z-lines [line0, line0 + nlines); partial sums -> partials[slot].
+// CG: spectrum loads bypass L1 (the fused Y/Z kernel reads rows other SMs
+// just wrote); DISCARD: the consumed spectrum rows are dropped from L2
+// without write-back (dead after this pass).
+template <class Cons, int L, bool CG = false, bool DISCARD = false>
+__device__ __forceinline__ void zinv_tile(const SpecView& sv, const double2* __restrict__ tw, int64_t line0,
+                                          int nlines, double scale, const Cons& cons, double* partials,
+                                          int64_t slot, bool discard = true) {
+  constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
+  extern __shared__ double2 sm[];
   const int nreal = 9 * nlines;
   const int npair = (nreal + 1) >> 1;
   const int nc = int(sv.n3c);
   const int ncr = (nc + 31) & ~31;  // warp-aligned k ranges (see zfwd_rr)
+  // the consumer's field rows of this block (read after the transform) go
+  // to L2 now, so the epilogue loads hit L2 instead of HBM latency
+  if (threadIdx.x < 9) cons.prefetch(int(threadIdx.x), line0 * N, int64_t(nlines) * N);
   __shared__ int64_t zr[kMaxZRows];
   for (int t = threadIdx.x; t < nreal; t += blockDim.x) zr[t] = sv.zrow(t % 9, line0 + t / 9);
   __syncthreads();
   // Hermitian completion of the pair (halfcomplex c2r: DC/Nyquist imaginary
   // parts ignored) into natural-order smem lines
-  for (int t = threadIdx.x; t < npair * ncr; t += blockDim.x) {
-    const int pp = t / ncr, k = t - pp * ncr;
-    if (k >= nc) continue;
-    const int rl = 2 * pp;
-    double2 xa = sv.spec[zr[rl] + k];
-    const double2 xb0 = make_double2(0.0, 0.0);
-    double2 xb = rl + 1 < nreal ? sv.spec[zr[rl + 1] + k] : xb0;
-    const bool selfconj = (k == 0) || (2 * k == N);
-    if (selfconj) {
-      xa.y = 0.0;
-      xb.y = 0.0;
+  // kZU rows of the loop are loaded before any is completed: 2 kZU
+  // independent 16-byte loads in flight per thread (one pair at a time left
+  // the pass latency-bound)
+  constexpr int kZU = 4;
+  const int total = npair * ncr;
+  for (int t0 = 0; t0 < total; t0 += kZU * int(blockDim.x)) {
+    double2 xa[kZU], xb[kZU];
+#pragma unroll
+    for (int r = 0; r < kZU; ++r) {
+      const int t = t0 + r * int(blockDim.x) + int(threadIdx.x);
+      const int pp = t / ncr, k = t - pp * ncr;
+      const int rl = 2 * pp;
+      xa[r] = xb[r] = make_double2(0.0, 0.0);
+      if (t < total && k < nc) {
+        if (CG) {
+          xa[r] = __ldcg(sv.spec + zr[rl] + k);
+          if (rl + 1 < nreal) xb[r] = __ldcg(sv.spec + zr[rl + 1] + k);
+        } else {
+          xa[r] = sv.spec[zr[rl] + k];
+          if (rl + 1 < nreal) xb[r] = sv.spec[zr[rl + 1] + k];
+        }
+      }
     }
-    sm[pp * LS + pad8(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
-    if (!selfconj) sm[pp * LS + pad8(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+#pragma unroll
+    for (int r = 0; r < kZU; ++r) {
+      const int t = t0 + r * int(blockDim.x) + int(threadIdx.x);
+      const int pp = t / ncr, k = t - pp * ncr;
+      if (t >= total || k >= nc) continue;
+      const bool selfconj = (k == 0) || (2 * k == N);
+      if (selfconj) {
+        xa[r].y = 0.0;
+        xb[r].y = 0.0;
+      }
+      sm[pp * LS + pad8(k)] = make_double2(xa[r].x - xb[r].y, xa[r].y + xb[r].x);
+      if (!selfconj) sm[pp * LS + pad8(N - k)] = make_double2(xa[r].x + xb[r].y, xb[r].x - xa[r].y);
+    }
   }
   __syncthreads();
+  if (DISCARD && discard) {
+    // every row of the tile has been read by the whole block (barrier above)
+    const int lpr = int((nc * 16 + 127) / 128);  // 128-byte lines per row (rows are 128-byte aligned)
+    for (int t = threadIdx.x; t < nreal * lpr; t += blockDim.x) {
+      const int rl = t / lpr, q = t - rl * lpr;
+      const char* a = reinterpret_cast<const char*>(sv.spec + zr[rl]) + 128 * q;
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+    }
+  }
   const int u = threadIdx.x % TL, p = threadIdx.x / TL;
   const bool active = p < npair;
   double2 v[1][8];
@@ -350,17 +391,28 @@ static __global__ void __launch_bounds__(512, 2)
   if constexpr (Cons::NSC > 0 || Cons::PERCOMP) {
     __syncthreads();  // sm reused for the group reduction
     group_reduce_store<Cons::NSC, Cons::PERCOMP>(sc, pa, pb, ca, active && hasb ? cb : -1, TL,
-                                                 reinterpret_cast<double*>(sm), partials, blockIdx.x);
+                                                 reinterpret_cast<double*>(sm), partials, slot);
   }
+}
+
+template <class Cons, int L>
+static __global__ void __launch_bounds__(512, 2)
+    zinv_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, double scale, Cons cons,
+            double* partials) {
+  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
+  const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
+  zinv_tile<Cons, L>(sv, tw, line0, int(min(int64_t(nl_per_block), nlines_tot - line0)), scale, cons, partials,
+                     blockIdx.x);
 }
 
 // ------------------------------------------------------------------ Y pass
 // W columns (lines) per block, thread -> (line = tid % W, u = tid / W)
-template <int L, bool INV, int MAXT = 512, int MINB = 2>
-static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
+// one tile: columns [kc0, kc0 + W) of component c, local plane i
+template <int L, bool INV, bool CG = false>
+__device__ __forceinline__ void ypass_tile(const SpecView& sv, const double2* __restrict__ tw, int W, int c,
+                                           int64_t i, int kc0) {
   constexpr int N = 1 << L;
   extern __shared__ double2 sm[];
-  const int c = blockIdx.z, i = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
@@ -368,7 +420,10 @@ static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const
   double2 v[1][8];
   if (active) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[0][q] = base[sv.rowA(i, rr_first_pos<L, false>(u, q))];
+    for (int q = 0; q < 8; ++q) {
+      const int64_t o = sv.rowA(i, rr_first_pos<L, false>(u, q));
+      v[0][q] = CG ? __ldcg(base + o) : base[o];
+    }
   }
   auto addr = [&](int, int pos) { return pad8(pos) * W + line; };
   rr_stages<L, INV, false, 0, 1>(v, u, active, sm, tw, addr);
@@ -376,6 +431,11 @@ static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const
 #pragma unroll
     for (int q = 0; q < 8; ++q) base[sv.rowA(i, rr_final_pos<L, false>(u, q))] = v[0][q];
   }
+}
+
+template <int L, bool INV, int MAXT = 512, int MINB = 2>
+static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
+  ypass_tile<L, INV>(sv, tw, W, blockIdx.z, blockIdx.y, blockIdx.x * W);
 }
 
 // Y pass with two columns per thread (columns line and line + W/2): twice the

@@ -592,6 +592,7 @@ struct ConsStore9 {
 #pragma unroll
     for (int c = 0; c < 9; ++c) dst[c * N + cell] = v[c];
   }
+  __device__ __forceinline__ void prefetch(int, int64_t, int64_t) const {}
   __device__ __forceinline__ double comp(int c, int64_t cell, double v, double*) const {
     dst[c * N + cell] = v;
     return 0.0;
@@ -621,6 +622,10 @@ struct ConsBasic {
   }
   static constexpr int NSC = 1;
   static constexpr bool PERCOMP = true;
+  // the old F rows of cells [cell0, cell0 + n) into L2 ahead of comp()
+  __device__ __forceinline__ void prefetch(int c, int64_t cell0, int64_t n) const {
+    bulk_prefetch_l2(fold + c * N + cell0, size_t(n) * 8);
+  }
   __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
     const double fn = fbar.v[c] - v / alpha;
     const double d = fn - (fold[c * N + cell] + fold_shift.v[c]);
@@ -645,6 +650,7 @@ struct ConsResid {
       acc[0] += v[c] * v[c];
     }
   }
+  __device__ __forceinline__ void prefetch(int, int64_t, int64_t) const {}
   __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
     r[c * N + cell] = -v;
     sc[0] += v * v;
@@ -667,6 +673,9 @@ struct ConsCg {
       ap[c * N + cell] = v[c];
       acc[0] += pdir[c * N + cell] * v[c];
     }
+  }
+  __device__ __forceinline__ void prefetch(int c, int64_t cell0, int64_t n) const {
+    bulk_prefetch_l2(pdir + c * N + cell0, size_t(n) * 8);
   }
   __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
     ap[c * N + cell] = v;
