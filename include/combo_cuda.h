@@ -12,6 +12,7 @@
  * Reference interface each group replaces:
  *   combo_solve ................. solve()                    src/solver.cpp:286-346, solver.hpp:68-69
  *   combo_stress_sweep .......... stress_sweep()             src/cell_material.cpp:104-168
+ *   combo_phase_averages ........ recover_phase_fields() + phase_averages()  src/postprocess.cpp:13-106
  *   combo_tangent_matvec ........ stress_sweep(tangents45) + tangent_matvec()  cell_material.cpp:170-194
  *   combo_tangent45 / _matvec45 . pack45 tangents / tangent_matvec (API compat) cell_material.cpp:86-102,170-194
  *   combo_project ............... GreenOperator::project()   src/green.cpp:133-151
@@ -111,6 +112,17 @@ typedef struct combo_sweep_stats {
   int64_t back_projections;
   int64_t laminate_iter_max;
 } combo_sweep_stats;
+
+/* PhaseAverages (postprocess.hpp:27-35) + RecoveredFields::max_resolve_iterations */
+typedef struct combo_phase_avg {
+  double pbar[9];
+  double pbar_plus[9];
+  double pbar_minus[9];
+  double c_plus;  /* inclusion volume fraction as represented */
+  int32_t has_plus;
+  int32_t has_minus;
+  int32_t max_resolve_iterations;
+} combo_phase_avg;
 
 /* NormalStats (normals.hpp:39-43) */
 typedef struct combo_normal_stats {
@@ -217,6 +229,9 @@ int combo_spectrum_bounds(combo_ctx* ctx, const double fbar[9], double* lo, doub
 /* --------------------------------------------------------------- operators */
 int combo_stress_sweep(combo_ctx* ctx, const double* F, double* P, combo_sweep_stats* stats, int mem);
 int combo_tangent_matvec(combo_ctx* ctx, const double* F, const double* x, double* y, int mem);
+/* post-solve: re-solve every composite laminate at F from its warm start
+ * (read only) and form the volume-weighted phase averages */
+int combo_phase_averages(combo_ctx* ctx, const double* F, combo_phase_avg* out, int mem);
 int combo_tangent45(combo_ctx* ctx, const double* F, double* t45, int mem);
 int combo_tangent45_matvec(combo_ctx* ctx, const double* t45, const double* x, double* y, int mem);
 int combo_project(combo_ctx* ctx, int green_kind, const double* in, double* out, int mem);

@@ -73,6 +73,7 @@ def lib():
         L.oracle_cm_stress_floor.restype = C.c_double
         L.oracle_cm_warm.argtypes = [C.c_void_p, _D, C.c_int]
         L.oracle_stress_sweep.argtypes = [C.c_void_p, _D, _D, C.c_void_p, _I64]
+        L.oracle_phase_averages.argtypes = [C.c_void_p, _D, _D]
         L.oracle_tangent_matvec.argtypes = [_D, _I64, _D, _D]
         L.oracle_dfmg_stress.argtypes = [C.c_void_p, _D, _D, _I64]
         L.oracle_dfmg_tangent.argtypes = [C.c_void_p, _D, _D, _D]
@@ -273,6 +274,15 @@ class CellMaterials:
         t = np.zeros(45 * self.n) if tangents else None
         lib().oracle_stress_sweep(self._h, F, P, t.ctypes.data_as(C.c_void_p) if tangents else None, st)
         return P, st, t
+
+    def phase_averages(self, F):
+        """recover_phase_fields + phase_averages (postprocess.cpp:13-106)."""
+        out = np.zeros(31)
+        if lib().oracle_phase_averages(self._h, _f64(F).ravel(), out) != 0:
+            raise RuntimeError(_err())
+        return dict(pbar=out[0:9].reshape(3, 3), pbar_plus=out[9:18].reshape(3, 3),
+                    pbar_minus=out[18:27].reshape(3, 3), c_plus=out[27], has_plus=bool(out[28]),
+                    has_minus=bool(out[29]), max_resolve_iterations=int(out[30]))
 
     def dfmg_stress(self, F):
         F = _f64(F).ravel()

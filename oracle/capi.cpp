@@ -266,6 +266,81 @@ int oracle_cm_warm(void* h, double* warm3, int set) {
   return 0;
 }
 
+// recover_phase_fields + phase_averages (postprocess.cpp:13-106).
+// out: pbar 9, pbar_plus 9, pbar_minus 9, c_plus, has_plus, has_minus,
+// max_resolve_iterations (31 doubles)
+int oracle_phase_averages(void* h, const double* F, double* out) {
+  try {
+    auto* H = static_cast<CmHandle*>(h);
+    CellMaterials& cm = H->cm;
+    Field9 f(cm.grid());
+    std::memcpy(f.data.data(), F, f.data.size() * sizeof(double));
+    // recover_phase_fields (postprocess.cpp:13-38): warm starts read only
+    const std::int64_t nid = cm.composite_cells();
+    std::vector<Mat3> pplus(static_cast<std::size_t>(nid)), pminus(static_cast<std::size_t>(nid));
+    std::vector<std::int64_t> cell_of(static_cast<std::size_t>(nid), -1);
+    for (std::int64_t i = 0; i < cm.cells(); ++i)
+      if (cm.cell_phase(std::size_t(i)) == 2) cell_of[std::size_t(cm.combo_id(std::size_t(i)))] = i;
+    int iter_max = 0;
+    for (std::int64_t id = 0; id < nid; ++id) {
+      const Mat3 fc = f.cell(std::size_t(cell_of[std::size_t(id)]));
+      const LaminateSolution sol =
+          finite_strain_solve(fc, cm.inclusion(), cm.matrix(), cm.meta(std::int32_t(id)),
+                              cm.warm_all()[std::size_t(id)], cm.laminate_options(), false);
+      pplus[std::size_t(id)] = sol.result.p_plus;
+      pminus[std::size_t(id)] = sol.result.p_minus;
+      iter_max = std::max(iter_max, sol.state.iterations);
+    }
+    // phase_averages (postprocess.cpp:49-106): chunk-4096 partials, fixed order
+    const std::int64_t n = cm.cells(), chunk = 4096, nch = (n + chunk - 1) / chunk;
+    Mat3 tps, tms;
+    double tpw = 0.0, tmw = 0.0;
+    for (std::int64_t c = 0; c < nch; ++c) {
+      Mat3 aps, ams;
+      double apw = 0.0, amw = 0.0;
+      for (std::int64_t i = c * chunk; i < std::min(n, (c + 1) * chunk); ++i) {
+        const std::uint8_t ph = cm.cell_phase(std::size_t(i));
+        if (ph == 2) {
+          const std::int32_t id = cm.combo_id(std::size_t(i));
+          const ComboMeta& m = cm.meta(id);
+          for (int q = 0; q < 9; ++q) {
+            aps.a[q] += m.c_plus * pplus[std::size_t(id)].a[q];
+            ams.a[q] += m.c_minus * pminus[std::size_t(id)].a[q];
+          }
+          apw += m.c_plus;
+          amw += m.c_minus;
+        } else {
+          Mat3 p;
+          law_eval(ph == 1 ? cm.inclusion() : cm.matrix(), f.cell(std::size_t(i)), p);
+          Mat3& acc = ph == 1 ? aps : ams;
+          for (int q = 0; q < 9; ++q) acc.a[q] += p.a[q];
+          (ph == 1 ? apw : amw) += 1.0;
+        }
+      }
+      for (int q = 0; q < 9; ++q) {
+        tps.a[q] += aps.a[q];
+        tms.a[q] += ams.a[q];
+      }
+      tpw += apw;
+      tmw += amw;
+    }
+    for (int q = 0; q < 9; ++q) {
+      const int i = q / 3, j = q % 3;
+      out[q] = (tps(i, j) + tms(i, j)) / double(n);
+      out[9 + q] = tpw > 0.0 ? tps(i, j) / tpw : 0.0;
+      out[18 + q] = tmw > 0.0 ? tms(i, j) / tmw : 0.0;
+    }
+    out[27] = tpw / double(n);
+    out[28] = tpw > 0.0;
+    out[29] = tmw > 0.0;
+    out[30] = iter_max;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // stress_sweep (cell_material.cpp:104-168); t45 nullable; stats4:
 // inadmissible, failures, back_projections, iter_max
 int oracle_stress_sweep(void* h, const double* F, double* P, double* t45, std::int64_t* stats4) {

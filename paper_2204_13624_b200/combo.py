@@ -61,6 +61,12 @@ class SweepStats(C.Structure):
                 ("back_projections", C.c_int64), ("laminate_iter_max", C.c_int64)]
 
 
+class PhaseAvg(C.Structure):  # combo_phase_avg (postprocess.hpp:27-35)
+    _fields_ = [("pbar", C.c_double * 9), ("pbar_plus", C.c_double * 9), ("pbar_minus", C.c_double * 9),
+                ("c_plus", C.c_double), ("has_plus", C.c_int32), ("has_minus", C.c_int32),
+                ("max_resolve_iterations", C.c_int32)]
+
+
 class NormalStats(C.Structure):
     _fields_ = [("composite", C.c_int64), ("degenerate_fallbacks", C.c_int64), ("too_few_fallbacks", C.c_int64)]
 
@@ -106,6 +112,7 @@ SIGNATURES = {
     "combo_set_warm_starts": (C.c_int, [_VP, _VP, C.c_int]),
     "combo_spectrum_bounds": (C.c_int, [_VP, _D, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "combo_stress_sweep": (C.c_int, [_VP, _VP, _VP, C.POINTER(SweepStats), C.c_int]),
+    "combo_phase_averages": (C.c_int, [_VP, _VP, C.POINTER(PhaseAvg), C.c_int]),
     "combo_tangent_matvec": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
     "combo_tangent45": (C.c_int, [_VP, _VP, _VP, C.c_int]),
     "combo_tangent45_matvec": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
@@ -479,6 +486,19 @@ class CellMaterials:
         st = SweepStats()
         self.ctx._check(self.ctx.L.combo_stress_sweep(self.ctx.h, _ptr(F), _ptr(P), C.byref(st), MEM_HOST))
         return P, (st.inadmissible_cells, st.laminate_failures, st.back_projections, st.laminate_iter_max)
+
+    def phase_averages(self, F):
+        """recover_phase_fields + phase_averages (postprocess.cpp:13-106) at the
+        converged F: composite laminates re-solved from the warm starts."""
+        o = PhaseAvg()
+        mem = _mem(F)
+        if mem == MEM_HOST:
+            F = _f64(F).ravel()
+        self.ctx._check(self.ctx.L.combo_phase_averages(self.ctx.h, _ptr(F), C.byref(o), mem))
+        m = lambda a: np.array(a[:]).reshape(3, 3)  # noqa: E731
+        return dict(pbar=m(o.pbar), pbar_plus=m(o.pbar_plus), pbar_minus=m(o.pbar_minus), c_plus=o.c_plus,
+                    has_plus=bool(o.has_plus), has_minus=bool(o.has_minus),
+                    max_resolve_iterations=int(o.max_resolve_iterations))
 
     def tangent_matvec(self, F, x):
         y = np.zeros(9 * self.n)

@@ -1973,6 +1973,50 @@ int combo_stress_sweep(combo_ctx* c, const double* F, double* P, combo_sweep_sta
   });
 }
 
+// recover_phase_fields + phase_averages (postprocess.cpp:13-106)
+int combo_phase_averages(combo_ctx* c, const double* F, combo_phase_avg* out, int mem) {
+  return guarded(c, [&] {
+    if (!out) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
+    require_bound(c);
+    require_single(c);
+    ensure_scratch(c);
+    const double* f = stage_in(c, F, mem, 0);
+    const size_t nc = size_t(std::max<int64_t>(c->ncomp, 1));
+    DBuf<double> pp, pm;
+    pp.alloc(9 * nc);
+    pm.alloc(9 * nc);
+    reset_stats(c);
+    if (c->ncomp > 0) {
+      const unsigned g = unsigned(std::min<int64_t>((c->ncomp + 127) / 128, int64_t(c->num_sms) * 64));
+      k_recover<<<g, 128, 0, c->stream>>>(c->mp, c->cell_data(), f, c->N, pp.p, pm.p, stats_ptr(c));
+      ++c->launches;
+      COMBO_CK(cudaGetLastError());
+    }
+    const int64_t nb = chunk_blocks(c);
+    double* part = part_ptr(c, nb, 20);
+    k_phase_sum<<<unsigned(nb), kEwThreads, 0, c->stream>>>(c->mp, c->cell_data(), f, c->N, pp.p, pm.p,
+                                                            chunks_of(c), part);
+    ++c->launches;
+    COMBO_CK(cudaGetLastError());
+    group_reduce(c, nb, 20, 0);
+    fetch_results(c);
+    const Stats* st = reinterpret_cast<const Stats*>(c->hres + 64);
+    if (st->inadmissible)
+      throw ComboError(COMBO_ERR_INADMISSIBLE_MACRO, "recover_phase_fields: det F_box <= 0 in a composite cell");
+    const double* r = c->hres;
+    const double n = double(c->Ng);
+    out->c_plus = r[9] / n;
+    out->has_plus = r[9] > 0.0;
+    out->has_minus = r[19] > 0.0;
+    for (int q = 0; q < 9; ++q) {
+      out->pbar_plus[q] = out->has_plus ? r[q] / r[9] : 0.0;
+      out->pbar_minus[q] = out->has_minus ? r[10 + q] / r[19] : 0.0;
+      out->pbar[q] = (r[q] + r[10 + q]) / n;
+    }
+    out->max_resolve_iterations = int32_t(st->iter_max);
+  });
+}
+
 int combo_tangent_matvec(combo_ctx* c, const double* F, const double* x, double* y, int mem) {
   return guarded(c, [&] {
     require_bound(c);

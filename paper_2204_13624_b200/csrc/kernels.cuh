@@ -203,6 +203,90 @@ static __global__ void __launch_bounds__(kEwThreads) k_sweep_pure(MatParams M, C
   block_reduce_store<9>(acc, partials, blockIdx.x);
 }
 
+// recover_phase_fields (postprocess.cpp:13-38): every composite re-solves
+// its laminate at F from the stored warm start (not written back); the
+// phase stresses P+ / P- of the returned state go to pp / pm [9][ncomp].
+static __global__ void __launch_bounds__(128) k_recover(MatParams M, CellData cd, const double* __restrict__ fin,
+                                                        int64_t N, double* __restrict__ pp, double* __restrict__ pm,
+                                                        Stats* st) {
+  unsigned long long inad = 0;
+  unsigned int itmax = 0;
+  for (int64_t id = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; id < cd.ncomp;
+       id += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t cell = cd.ccell[id];
+    double f[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell];
+    const double n[3] = {cd.nrm[id], cd.nrm[cd.ncomp + id], cd.nrm[2 * cd.ncomp + id]};
+    const double a0[3] = {cd.warm[id], cd.warm[cd.ncomp + id], cd.warm[2 * cd.ncomp + id]};
+    LamResult R;
+    laminate_solve(M, f, n, cd.cp[id], cd.cm[id], a0, R);
+    double fp[9], fm[9], p1[9], p2[9];
+    if (R.inadmissible) {
+      ++inad;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) p1[c] = p2[c] = 0.0;
+    } else {
+      itmax = max(itmax, (unsigned)R.iterations);
+      // the phases of the returned state, as the last update_phases
+      form_phases(f, n, cd.cp[id], cd.cm[id], R.a, fp, fm);
+      NhState s1, s2;
+      if (!law_eval(M.law[1], fp, p1, s1))
+#pragma unroll
+        for (int c = 0; c < 9; ++c) p1[c] = 0.0;
+      if (!law_eval(M.law[0], fm, p2, s2))
+#pragma unroll
+        for (int c = 0; c < 9; ++c) p2[c] = 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      pp[c * cd.ncomp + id] = p1[c];
+      pm[c * cd.ncomp + id] = p2[c];
+    }
+  }
+  warp_stats(st, inad, 0, 0, itmax);
+}
+
+// phase_averages (postprocess.cpp:49-106): chunk partials of
+// [sum+ (9), weight+, sum- (9), weight-]
+static __global__ void __launch_bounds__(kEwThreads) k_phase_sum(MatParams M, CellData cd,
+                                                                 const double* __restrict__ fin, int64_t N,
+                                                                 const double* __restrict__ pp,
+                                                                 const double* __restrict__ pm, Chunks ch,
+                                                                 double* partials) {
+  double acc[20];
+#pragma unroll
+  for (int c = 0; c < 20; ++c) acc[c] = 0.0;
+  int64_t beg, end;
+  chunk_range(ch, beg, end);
+  for (int64_t cell = beg + threadIdx.x; cell < end; cell += blockDim.x) {
+    const int32_t id = cd.cid[cell];
+    if (id >= 0) {
+      const double cpl = cd.cp[id], cmi = cd.cm[id];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        acc[c] += cpl * pp[c * cd.ncomp + id];
+        acc[10 + c] += cmi * pm[c * cd.ncomp + id];
+      }
+      acc[9] += cpl;
+      acc[19] += cmi;
+    } else {
+      double f[9], p[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell];
+      NhState s;
+      if (!law_eval(id == -2 ? M.law[1] : M.law[0], f, p, s))
+#pragma unroll
+        for (int c = 0; c < 9; ++c) p[c] = 0.0;
+      const int o = id == -2 ? 0 : 10;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) acc[o + c] += p[c];
+      acc[o + 9] += 1.0;
+    }
+  }
+  block_reduce_store<20>(acc, partials, blockIdx.x);
+}
+
 // CG step P1 (solver.cpp:186-197, deferred): x += step_prev * pdir_old (the
 // x update of the previous iteration, applied where pdir_old is read anyway),
 // pdir = first ? r : r + beta * pdir_old ; y = A(F) : pdir (matrix free NH,

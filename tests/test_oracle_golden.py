@@ -245,3 +245,47 @@ def test_c7_reference_pbar_fixture():
     ref = np.array(d["ref_pbar"]).reshape(3, 3)
     assert [round(ref[0, 0], 4), round(ref[0, 1], 4), round(ref[1, 0], 4), round(ref[1, 1], 4)] == [
         0.0007, 0.3724, 0.3667, 0.0115]
+
+
+# ------------------------------------------------ post-processing (§8f #1)
+def _post_sphere(oracle):
+    img = oracle.generate("sphere", (32, 32, 32), (1, 1, 1), 0.4)
+    kind, cp, _ = oracle.coarsen(img, (4, 4, 4))
+    nrm, _, _ = oracle.normals(img, (4, 4, 4))
+    return kind, cp, nrm
+
+
+def test_phase_recovery_partition_identity(oracle):
+    """test_postprocess.cpp:31-67: recovery within 1 iteration, idempotent,
+    c+ P+ + c- P- = P, postprocess P equals the solver's P, exact c+."""
+    kind, cp, nrm = _post_sphere(oracle)
+    soft, stiff = oracle.neo_hookean_enu(1.0, 0.0), oracle.neo_hookean_enu(10.0, 0.3)
+    cm = oracle.CellMaterials((8, 8, 8), kind, cp, nrm, soft, stiff)
+    f = np.eye(3)
+    f[0, 1] = 0.3
+    r = cm.solve(f, scheme=1, green=1, tol=1e-9)
+    assert r["report"]["success"]
+    pa = cm.phase_averages(r["f"])
+    pa2 = cm.phase_averages(r["f"])
+    assert pa["max_resolve_iterations"] <= 1
+    assert np.array_equal(pa["pbar_plus"], pa2["pbar_plus"]) and np.array_equal(pa["pbar_minus"], pa2["pbar_minus"])
+    assert pa["has_plus"] and pa["has_minus"]
+    rec = pa["c_plus"] * pa["pbar_plus"] + (1.0 - pa["c_plus"]) * pa["pbar_minus"]
+    assert np.linalg.norm(rec - pa["pbar"]) <= 1e-12 * np.linalg.norm(pa["pbar"])
+    assert np.linalg.norm(pa["pbar"] - r["pbar"]) <= 1e-10 * np.linalg.norm(r["pbar"])
+    assert abs(pa["c_plus"] - cm.represented_c_plus) <= 1e-13
+
+
+def test_phase_averages_all_matrix(oracle):
+    """test_postprocess.cpp:69-84: no inclusion average on an all-matrix RVE."""
+    kind = np.zeros(64, np.uint8)
+    cp = np.zeros(64)
+    soft, stiff = oracle.neo_hookean_enu(1.0, 0.0), oracle.neo_hookean_enu(10.0, 0.3)
+    cm = oracle.CellMaterials((4, 4, 4), kind, cp, np.zeros(3 * 64), soft, stiff)
+    f = np.eye(3)
+    f[0, 1] = 0.2
+    r = cm.solve(f, scheme=1, green=1, tol=1e-8)
+    assert r["report"]["success"]
+    pa = cm.phase_averages(r["f"])
+    assert not pa["has_plus"] and pa["has_minus"]
+    assert np.linalg.norm(pa["pbar_minus"] - pa["pbar"]) <= 1e-14 * np.linalg.norm(pa["pbar"])
