@@ -41,6 +41,19 @@ LS_MODEL = {  # algorithmic bytes per boxel per LS iteration
 }
 
 
+def ncu_traffic(kernel, grid):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
+    `kernel` from the committed ncu --set full capture, when it was taken on
+    this grid (profiles/ncu_traffic.json); None otherwise."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p)).get(kernel)
+    if not d or list(d.get("grid", [])) != list(grid):
+        return None
+    return d
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -359,7 +372,10 @@ def main():
                        else "single GPU",
                        "preprocess_s": t_pre},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak,
+                         "traffic": (ncu_traffic(dname, dims) or {}).get("traffic_bytes_per_launch"),
+                         "traffic_source": (ncu_traffic(dname, dims) or {}).get("source"),
+                         "peak_kind": peak_kind,
                          "bytes_per_launch": per_launch_bytes, "avg_ms": avg_s * 1000.0},
             "ls_roofline": {"model_bytes_per_boxel_iter": model_bytes / (N * ls_total) if ls_total else None,
                             "achieved": ls_achieved, "peak": peak, "unit": "GB/s",
