@@ -1,2 +1,6 @@
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_r1d.log 2>&1; echo "rc $?" >> gpurun_out/pytest_gpu_r1d.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r1d.log 2>&1; echo "smoke rc $?" >> gpurun_out/smoke_r1d.log
+bash tools/ab_bench.sh base > gpurun_out/ab2.txt 2>&1
+bash tools/ab_bench.sh xw8 COMBO_XW=8 >> gpurun_out/ab2.txt 2>&1
+bash tools/ab_bench.sh xw2 COMBO_XW=2 >> gpurun_out/ab2.txt 2>&1
+bash tools/ab_bench.sh yw8 COMBO_YW=8 >> gpurun_out/ab2.txt 2>&1
+bash tools/ab_bench.sh yw2 COMBO_YW=2 >> gpurun_out/ab2.txt 2>&1
+bash tools/ab_bench.sh zl2 COMBO_ZLINES=2 >> gpurun_out/ab2.txt 2>&1
