@@ -7,6 +7,7 @@
 //   ComboGrid coarsen(img, factors)                      combo_grid.hpp:62-63
 //   NormalStats compute_normals(img, grid, method, opt)  normals.hpp:55-57
 //   SolveResult solve(cm, fbar, cfg)                     solver.hpp:68-69
+//   PhaseAverages phase_averages(f, cm)                  postprocess.hpp:20-35
 //
 // Differences from the reference API, all forced by the boundary:
 //   * plain std::array / std::vector instead of Eigen types;
@@ -188,6 +189,30 @@ inline combo_sweep_stats stress_sweep(CellMaterials& cm, const Field9& f, Field9
   combo_sweep_stats st{};
   check(combo_stress_sweep(cm.device().get(), f.data.data(), p.data.data(), &st, COMBO_MEM_HOST), cm.device().get());
   return st;
+}
+
+/// recover_phase_fields + phase_averages (postprocess.cpp:13-106) in one
+/// call: composite laminates re-solved at f from the warm starts (read only).
+struct PhaseAverages {  // postprocess.hpp:27-35
+  Mat3 pbar{}, pbar_plus{}, pbar_minus{};
+  bool has_plus = false, has_minus = false;
+  double c_plus = 0.0;
+  int max_resolve_iterations = 0;
+};
+inline PhaseAverages phase_averages(const Field9& f, CellMaterials& cm) {
+  combo_phase_avg a{};
+  check(combo_phase_averages(cm.device().get(), f.data.data(), &a, COMBO_MEM_HOST), cm.device().get());
+  PhaseAverages o;
+  for (int q = 0; q < 9; ++q) {
+    o.pbar[q] = a.pbar[q];
+    o.pbar_plus[q] = a.pbar_plus[q];
+    o.pbar_minus[q] = a.pbar_minus[q];
+  }
+  o.has_plus = a.has_plus != 0;
+  o.has_minus = a.has_minus != 0;
+  o.c_plus = a.c_plus;
+  o.max_resolve_iterations = a.max_resolve_iterations;
+  return o;
 }
 
 /// y = A(F) : x with the tangent of the last sweep's states (matrix free;
