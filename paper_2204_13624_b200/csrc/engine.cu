@@ -201,6 +201,7 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->pipe_y = knob("COMBO_PIPE_Y", 0) != 0;
   p->pipe_x = knob("COMBO_PIPE_X", 0) != 0;
   p->xv = knob("COMBO_XV", 4);
+  p->xminb = knob("COMBO_XMINB", 2);
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
