@@ -1,0 +1,48 @@
+"""Staged pipeline generate -> coarsen -> normals -> solve -> post on the
+device (runconfig.py, tools/combo_main.cpp:84-245): artifacts equal the
+oracle's bit for bit (image, grid), the solve from the staged files equals a
+direct CellMaterials solve bitwise, the phase averages of `post` at the
+dumped F equal those of `solve`."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_pipeline_stages(ctx, oracle, tmp_path):
+    from paper_2204_13624_b200 import CellMaterials, neo_hookean_enu
+    from paper_2204_13624_b200 import io as cio
+    from paper_2204_13624_b200 import runconfig as rc
+
+    cfg = rc.RunConfig.from_json({
+        "geometry": {"shape": "sphere", "radius": 0.3}, "dims": [32, 32, 32], "coarsen": [4, 4, 4],
+        "loading": [[1.0, 0.2, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]],
+        "solver": {"scheme": "newton_cg", "green": "rotated", "tol_equilibrium": 1e-9, "load_steps": 2},
+        "output": {"dir": str(tmp_path), "dump_fields": True, "slices": [{"component": 1, "axis": 2, "index": 3}]},
+    })
+    img = rc.stage_generate(ctx, cfg)
+    assert np.array_equal(img.data, oracle.generate("sphere", (32, 32, 32), (1, 1, 1), 0.3))
+    rc.stage_coarsen(ctx, cfg)
+    assert cio.read_json(tmp_path / "coarsen_report.json")["volume_fraction_exact"]
+    grid = rc.stage_normals(ctx, cfg)
+    ko, cpo, _ = oracle.coarsen(img.data, (4, 4, 4))
+    no, fo, _ = oracle.normals(img.data, (4, 4, 4))
+    g2 = cio.load_grid(tmp_path / "grid.json")
+    assert np.array_equal(g2.kind, ko) and np.array_equal(g2.c_plus, cpo) and np.array_equal(g2.normal, no)
+    assert np.array_equal(grid.normal_flag, fo)
+
+    r, rep = rc.stage_solve(ctx, cfg)
+    assert rep["report"]["success"] and len(rep["report"]["steps"]) == 2
+    direct = CellMaterials(ctx, g2.dims, ko, cpo, no, neo_hookean_enu(1.0, 0.0), neo_hookean_enu(10.0, 0.3))
+    rd = direct.solve(cfg.loading, cfg.solver_config())
+    assert np.array_equal(np.asarray(rd["f"]), np.asarray(r["f"]))
+    assert np.allclose(rep["averages"]["pbar"], rd["pbar"], rtol=1e-9, atol=1e-14)
+    F, dims, _ = cio.load_field(tmp_path / "F.json")
+    assert dims == (8, 8, 8) and np.array_equal(F.ravel(), np.asarray(r["f"]).ravel())
+
+    rc.stage_post(ctx, cfg)
+    av = cio.read_json(tmp_path / "averages.json")
+    assert np.allclose(av["pbar"], rep["averages"]["pbar"], rtol=1e-8, atol=1e-14)  # re-solved from cold warm starts
+    assert (tmp_path / "slice_0.raw").stat().st_size == 8 * 8 * 8
+    for s in ("generate", "coarsen", "normals", "solve", "post"):
+        assert (tmp_path / f"config_effective.{s}.json").exists()

@@ -1,0 +1,82 @@
+"""RunConfig / make_material / apply_override (paper_2204_13624_b200/runconfig.py),
+CPU only; mirrors test_config.cpp:11-78 of the reference."""
+import pytest
+
+from paper_2204_13624_b200 import runconfig as rc
+
+
+def test_defaults_and_echo_round_trip():
+    # test_config.cpp:11-24
+    c = rc.RunConfig.from_json({})
+    assert c.solver["scheme"] == "newton_cg"
+    assert c.solver["green"] == "rotated"
+    assert c.loading[0, 1] == 0.5
+    assert c.laminate["tol_rel"] == 1e-10
+    assert c.solver["tol_equilibrium"] == 1e-8
+    echo = c.to_json()
+    assert rc.RunConfig.from_json(echo).to_json() == echo
+
+
+def test_unknown_keys_rejected_everywhere():
+    # test_config.cpp:26-37
+    for j in ({"bogus": 1}, {"solver": {"schem": "basic"}}, {"normals": {"methodd": "barycenter"}},
+              {"geometry": {"shape": "sphere", "r": 1}}, {"laminate": {"tol": 1}}, {"output": {"dirr": "x"}},
+              {"materials": {"fiber": {}}}):
+        with pytest.raises(rc.ConfigInvalid):
+            rc.RunConfig.from_json(j)
+
+
+def test_invalid_values_rejected():
+    # test_config.cpp:39-49 and SolverConfig::validate (solver.cpp:277-284)
+    for j in ({"loading": [[-1, 0, 0], [0, 1, 0], [0, 0, 1]]},
+              {"solver": {"material_eval": "dfmg", "green": "rotated"}}, {"solver": {"scheme": "x"}},
+              {"solver": {"load_steps": 0}}, {"solver": {"tol_equilibrium": 0.0}}, {"normals": {"conv": "x"}},
+              {"geometry": {"radius": 0.3}}):
+        with pytest.raises(rc.ConfigInvalid):
+            rc.RunConfig.from_json(j)
+    with pytest.raises(rc.BadShapeSpec):
+        rc.RunConfig.from_json({"geometry": {"shape": "moebius"}})
+    c = rc.RunConfig.from_json({"solver": {"material_eval": "dfmg", "green": "staggered"}})
+    assert c.solver["material_eval"] == "dfmg"
+
+
+def test_material_factory():
+    # test_config.cpp:51-62 (law structs of the C-ABI; no GPU needed)
+    nh = rc.make_material({"model": "neo_hookean", "E": 10.0, "nu": 0.3})
+    assert nh.kind == 0 and abs(nh.mu - 10.0 / 2.6) < 1e-15
+    lin = rc.make_material({"model": "linear", "E": 1.0, "nu": 0.0})
+    assert lin.kind == 1 and lin.c6[0] == 1.0
+    with pytest.raises(rc.ConfigInvalid):
+        rc.make_material({"model": "thermal", "kappa": [[1, 0, 0], [0, 1, 0], [0, 0, 1]]})
+    with pytest.raises(rc.ConfigInvalid):
+        rc.make_material({"model": "squishy"})
+    with pytest.raises(rc.ConfigInvalid):
+        rc.make_material({"model": "neo_hookean", "E": 1.0, "nu": 0.2, "G": 3})
+
+
+def test_overrides_with_dot_paths():
+    # test_config.cpp:64-74
+    j = {}
+    rc.apply_override(j, "solver.scheme=basic")
+    rc.apply_override(j, "solver.tol_equilibrium=1e-6")
+    rc.apply_override(j, "dims=[8,8,8]")
+    c = rc.RunConfig.from_json(j)
+    assert c.solver["scheme"] == "basic"
+    assert c.solver["tol_equilibrium"] == 1e-6
+    assert c.dims[0] == 8
+    with pytest.raises(rc.ConfigInvalid):
+        rc.apply_override(j, "no_equals_sign")
+    with pytest.raises(rc.ConfigInvalid):
+        rc.apply_override(j, "solver..x=1")
+
+
+def test_missing_upstream_artifacts(tmp_path):
+    # combo_main.cpp: stages fail with UpstreamArtifactMissing before touching the device
+    c = rc.RunConfig.from_json({"output": {"dir": str(tmp_path / "o")}})
+    with pytest.raises(rc.UpstreamArtifactMissing):
+        rc.stage_solve(None, c)
+    with pytest.raises(rc.UpstreamArtifactMissing):
+        rc.stage_post(None, c)
+    with pytest.raises(rc.UpstreamArtifactMissing):
+        rc.stage_normals(None, c)
+    assert (tmp_path / "o" / "config_effective.solve.json").exists()
