@@ -13,6 +13,7 @@
  *   combo_solve ................. solve()                    src/solver.cpp:286-346, solver.hpp:68-69
  *   combo_stress_sweep .......... stress_sweep()             src/cell_material.cpp:104-168
  *   combo_phase_averages ........ recover_phase_fields() + phase_averages()  src/postprocess.cpp:13-106
+ *   combo_recover_composites .... recover_phase_fields() per composite       src/postprocess.cpp:13-36
  *   combo_tangent_matvec ........ stress_sweep(tangents45) + tangent_matvec()  cell_material.cpp:170-194
  *   combo_tangent45 / _matvec45 . pack45 tangents / tangent_matvec (API compat) cell_material.cpp:86-102,170-194
  *   combo_project ............... GreenOperator::project()   src/green.cpp:133-151
@@ -232,6 +233,14 @@ int combo_tangent_matvec(combo_ctx* ctx, const double* F, const double* x, doubl
 /* post-solve: re-solve every composite laminate at F from its warm start
  * (read only) and form the volume-weighted phase averages */
 int combo_phase_averages(combo_ctx* ctx, const double* F, combo_phase_avg* out, int mem);
+/* recover_phase_fields() per composite cell (src/postprocess.cpp:13-36), the
+ * inputs of interface_tractions() (src/postprocess.cpp:114-141): for composite
+ * id q < combo_composite_cells(): cell[q] (flat boxel index), f_plus /
+ * f_minus [9][ncomp] (component-major F+ / F-), traction [3][ncomp]
+ * (LaminateResult::traction, src/laminate.cpp:266). Buffers are host or
+ * device memory per `mem`. */
+int combo_recover_composites(combo_ctx* ctx, const double* F, int64_t* cell, double* f_plus, double* f_minus,
+                             double* traction, int mem);
 int combo_tangent45(combo_ctx* ctx, const double* F, double* t45, int mem);
 int combo_tangent45_matvec(combo_ctx* ctx, const double* t45, const double* x, double* y, int mem);
 int combo_project(combo_ctx* ctx, int green_kind, const double* in, double* out, int mem);

@@ -113,6 +113,7 @@ SIGNATURES = {
     "combo_spectrum_bounds": (C.c_int, [_VP, _D, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "combo_stress_sweep": (C.c_int, [_VP, _VP, _VP, C.POINTER(SweepStats), C.c_int]),
     "combo_phase_averages": (C.c_int, [_VP, _VP, C.POINTER(PhaseAvg), C.c_int]),
+    "combo_recover_composites": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int]),
     "combo_tangent_matvec": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
     "combo_tangent45": (C.c_int, [_VP, _VP, _VP, C.c_int]),
     "combo_tangent45_matvec": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int]),
@@ -499,6 +500,29 @@ class CellMaterials:
         return dict(pbar=m(o.pbar), pbar_plus=m(o.pbar_plus), pbar_minus=m(o.pbar_minus), c_plus=o.c_plus,
                     has_plus=bool(o.has_plus), has_minus=bool(o.has_minus),
                     max_resolve_iterations=int(o.max_resolve_iterations))
+
+    def recover_composites(self, F):
+        """recover_phase_fields per composite (postprocess.cpp:13-36) ->
+        dict(cell (nc,), f_plus / f_minus (nc, 3, 3), traction (nc, 3))"""
+        nc = self.composites
+        mem = _mem(F)
+        if mem == MEM_HOST:
+            F = _f64(F).ravel()
+        cell = np.zeros(max(nc, 1), np.int64)
+        fp, fm, tr = np.zeros(9 * max(nc, 1)), np.zeros(9 * max(nc, 1)), np.zeros(3 * max(nc, 1))
+        if mem != MEM_HOST:
+            import torch
+
+            dev = F.device
+            cell = torch.from_numpy(cell).to(dev)
+            fp, fm, tr = (torch.from_numpy(a).to(dev) for a in (fp, fm, tr))
+        self.ctx._check(self.ctx.L.combo_recover_composites(self.ctx.h, _ptr(F), _ptr(cell), _ptr(fp), _ptr(fm),
+                                                            _ptr(tr), mem))
+        if mem != MEM_HOST:
+            cell, fp, fm, tr = (a.cpu().numpy() for a in (cell, fp, fm, tr))
+        sl = max(nc, 1)
+        return dict(cell=cell[:nc], f_plus=fp.reshape(9, sl)[:, :nc].T.reshape(nc, 3, 3),
+                    f_minus=fm.reshape(9, sl)[:, :nc].T.reshape(nc, 3, 3), traction=tr.reshape(3, sl)[:, :nc].T)
 
     def tangent_matvec(self, F, x):
         y = np.zeros(9 * self.n)

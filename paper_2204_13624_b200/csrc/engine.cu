@@ -2018,6 +2018,52 @@ int combo_phase_averages(combo_ctx* c, const double* F, combo_phase_avg* out, in
   });
 }
 
+// recover_phase_fields per composite (postprocess.cpp:13-36) for
+// interface_tractions (postprocess.cpp:114-141): component-major outputs by
+// composite id, device or host buffers per `mem`
+int combo_recover_composites(combo_ctx* c, const double* F, int64_t* cell, double* f_plus, double* f_minus,
+                             double* traction, int mem) {
+  return guarded(c, [&] {
+    require_bound(c);
+    require_single(c);
+    ensure_scratch(c);
+    const double* f = stage_in(c, F, mem, 0);
+    const size_t nc = size_t(std::max<int64_t>(c->ncomp, 1));
+    if (c->ncomp == 0) return;
+    if (!cell || !f_plus || !f_minus || !traction) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
+    DBuf<int64_t> dcell;
+    DBuf<double> dfp, dfm, dtr;
+    const bool host = mem == COMBO_MEM_HOST;
+    int64_t* oc = cell;
+    double *ofp = f_plus, *ofm = f_minus, *otr = traction;
+    if (host) {
+      dcell.alloc(nc);
+      dfp.alloc(9 * nc);
+      dfm.alloc(9 * nc);
+      dtr.alloc(3 * nc);
+      oc = dcell.p;
+      ofp = dfp.p;
+      ofm = dfm.p;
+      otr = dtr.p;
+    }
+    reset_stats(c);
+    const unsigned g = unsigned(std::min<int64_t>((c->ncomp + 127) / 128, int64_t(c->num_sms) * 64));
+    k_recover_state<<<g, 128, 0, c->stream>>>(c->mp, c->cell_data(), f, c->N, oc, ofp, ofm, otr, stats_ptr(c));
+    ++c->launches;
+    COMBO_CK(cudaGetLastError());
+    fetch_results(c);
+    const Stats* st = reinterpret_cast<const Stats*>(c->hres + 64);
+    if (st->inadmissible)
+      throw ComboError(COMBO_ERR_INADMISSIBLE_MACRO, "recover_phase_fields: det F_box <= 0 in a composite cell");
+    if (host) {
+      COMBO_CK(cudaMemcpy(cell, oc, nc * sizeof(int64_t), cudaMemcpyDeviceToHost));
+      COMBO_CK(cudaMemcpy(f_plus, ofp, 9 * nc * sizeof(double), cudaMemcpyDeviceToHost));
+      COMBO_CK(cudaMemcpy(f_minus, ofm, 9 * nc * sizeof(double), cudaMemcpyDeviceToHost));
+      COMBO_CK(cudaMemcpy(traction, otr, 3 * nc * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
 int combo_tangent_matvec(combo_ctx* c, const double* F, const double* x, double* y, int mem) {
   return guarded(c, [&] {
     require_bound(c);

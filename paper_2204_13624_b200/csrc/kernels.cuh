@@ -206,6 +206,61 @@ static __global__ void __launch_bounds__(kEwThreads) k_sweep_pure(MatParams M, C
 // recover_phase_fields (postprocess.cpp:13-38): every composite re-solves
 // its laminate at F from the stored warm start (not written back); the
 // phase stresses P+ / P- of the returned state go to pp / pm [9][ncomp].
+// per-composite recovered laminate state for interface tractions
+// (recover_phase_fields, postprocess.cpp:13-36; LaminateResult traction,
+// laminate.cpp:258-266): F+, F- and T = P+ n (converged) or the mean of the
+// two phase tractions (best iterate), by composite id
+static __global__ void __launch_bounds__(128) k_recover_state(MatParams M, CellData cd, const double* __restrict__ fin,
+                                                              int64_t N, int64_t* __restrict__ cell_out,
+                                                              double* __restrict__ fpo, double* __restrict__ fmo,
+                                                              double* __restrict__ tro, Stats* st) {
+  unsigned long long inad = 0;
+  unsigned int itmax = 0;
+  for (int64_t id = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; id < cd.ncomp;
+       id += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t cell = cd.ccell[id];
+    double f[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) f[c] = fin[c * N + cell];
+    const double n[3] = {cd.nrm[id], cd.nrm[cd.ncomp + id], cd.nrm[2 * cd.ncomp + id]};
+    const double a0[3] = {cd.warm[id], cd.warm[cd.ncomp + id], cd.warm[2 * cd.ncomp + id]};
+    LamResult R;
+    laminate_solve(M, f, n, cd.cp[id], cd.cm[id], a0, R);
+    double fp[9], fm[9], p1[9], p2[9], t[3];
+    if (R.inadmissible) {
+      ++inad;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) fp[c] = fm[c] = 0.0;
+      t[0] = t[1] = t[2] = 0.0;
+    } else {
+      itmax = max(itmax, (unsigned)R.iterations);
+      form_phases(f, n, cd.cp[id], cd.cm[id], R.a, fp, fm);
+      NhState s1, s2;
+      if (!law_eval(M.law[1], fp, p1, s1))
+#pragma unroll
+        for (int c = 0; c < 9; ++c) p1[c] = 0.0;
+      if (!law_eval(M.law[0], fm, p2, s2))
+#pragma unroll
+        for (int c = 0; c < 9; ++c) p2[c] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double tp = p1[3 * i] * n[0] + p1[3 * i + 1] * n[1] + p1[3 * i + 2] * n[2];
+        const double tm = p2[3 * i] * n[0] + p2[3 * i + 1] * n[1] + p2[3 * i + 2] * n[2];
+        t[i] = R.converged ? tp : 0.5 * (tp + tm);
+      }
+    }
+    cell_out[id] = cell;
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      fpo[c * cd.ncomp + id] = fp[c];
+      fmo[c * cd.ncomp + id] = fm[c];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) tro[i * cd.ncomp + id] = t[i];
+  }
+  warp_stats(st, inad, 0, 0, itmax);
+}
+
 static __global__ void __launch_bounds__(128) k_recover(MatParams M, CellData cd, const double* __restrict__ fin,
                                                         int64_t N, double* __restrict__ pp, double* __restrict__ pm,
                                                         Stats* st) {

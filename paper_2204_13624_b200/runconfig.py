@@ -13,8 +13,9 @@ Artifacts are the reference's (`image.json`, `grid.json`, `solve_report.json`,
 `config_effective.<stage>.json`) in the same formats (io.py). Every stage
 runs on the device through the C-ABI: generation, coarsening and normals
 (`Context.generate/coarsen/compute_normals`), the solve and the phase
-averages. Out of scope: interface-traction CSV and facet export (post),
-`bench` tables, and the fiber / cross-ply / fiber-pack generators (not on
+averages and the per-composite laminate recovery behind the traction CSV
+(facet geometry is host arithmetic, facets.py). Out of scope: `bench` tables,
+the argv front end, and the fiber / cross-ply / fiber-pack generators (not on
 the device path; `generate` raises ConfigInvalid for them).
 """
 from __future__ import annotations
@@ -379,8 +380,8 @@ def stage_solve(ctx, cfg):
 
 
 def stage_post(ctx, cfg):
-    """cmd_post (combo_main.cpp:212-245) without the traction CSV: phase
-    averages at the dumped F and the configured slices."""
+    """cmd_post (combo_main.cpp:212-245): phase averages at the dumped F,
+    facet export + interface tractions (tractions.csv), configured slices."""
     _echo(cfg, "post")
     gp, fp = _artifact(cfg, "grid.json"), _artifact(cfg, "F.json")
     if not os.path.exists(gp):
@@ -392,6 +393,11 @@ def stage_post(ctx, cfg):
     cm = _cell_materials(ctx, cfg, grid)
     pa = cm.phase_averages(f.ravel())
     cio.write_json(cio.phase_averages_to_json(pa), _artifact(cfg, "averages.json"))
+    from . import facets as fx
+
+    facets = fx.facet_export(grid.dims, grid.lengths, grid.kind, grid.c_plus, grid.normal)
+    samples = fx.interface_tractions(cm.recover_composites(f.ravel()), facets, grid.dims)
+    fx.write_traction_csv(samples, _artifact(cfg, "tractions.csv"))
     for n, s in enumerate(cfg.slices):
         cio.save_slice(f, dims, int(s.get("component", 1)), int(s.get("axis", 2)), int(s.get("index", 0)),
                        _artifact(cfg, f"slice_{n}.json"))

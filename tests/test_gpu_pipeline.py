@@ -44,5 +44,7 @@ def test_pipeline_stages(ctx, oracle, tmp_path):
     av = cio.read_json(tmp_path / "averages.json")
     assert np.allclose(av["pbar"], rep["averages"]["pbar"], rtol=1e-8, atol=1e-14)  # re-solved from cold warm starts
     assert (tmp_path / "slice_0.raw").stat().st_size == 8 * 8 * 8
+    rows = (tmp_path / "tractions.csv").read_text().splitlines()
+    assert len(rows) - 1 == int(np.count_nonzero((g2.kind == 2) & (np.linalg.norm(g2.normal, axis=1) > 0)))
     for s in ("generate", "coarsen", "normals", "solve", "post"):
         assert (tmp_path / f"config_effective.{s}.json").exists()
