@@ -215,6 +215,34 @@ inline PhaseAverages phase_averages(const Field9& f, CellMaterials& cm) {
   return o;
 }
 
+/// recover_phase_fields per composite (postprocess.cpp:13-36): the
+/// LaminateResult fields interface_tractions() consumes, by composite id.
+struct RecoveredComposite {
+  int64_t cell = 0;
+  Mat3 f_plus{}, f_minus{};
+  double traction[3] = {0.0, 0.0, 0.0};
+};
+inline std::vector<RecoveredComposite> recover_composites(const Field9& f, CellMaterials& cm) {
+  int64_t nc = 0;
+  check(combo_composite_cells(cm.device().get(), &nc), cm.device().get());
+  const size_t n = size_t(nc > 0 ? nc : 1);
+  std::vector<int64_t> cell(n);
+  std::vector<double> fp(9 * n), fm(9 * n), tr(3 * n);
+  check(combo_recover_composites(cm.device().get(), f.data.data(), cell.data(), fp.data(), fm.data(), tr.data(),
+                                 COMBO_MEM_HOST),
+        cm.device().get());
+  std::vector<RecoveredComposite> out(static_cast<size_t>(nc));
+  for (size_t q = 0; q < out.size(); ++q) {
+    out[q].cell = cell[q];
+    for (int c = 0; c < 9; ++c) {
+      out[q].f_plus[c] = fp[size_t(c) * n + q];
+      out[q].f_minus[c] = fm[size_t(c) * n + q];
+    }
+    for (int i = 0; i < 3; ++i) out[q].traction[i] = tr[size_t(i) * n + q];
+  }
+  return out;
+}
+
 /// y = A(F) : x with the tangent of the last sweep's states (matrix free;
 /// replaces stress_sweep(tangents45) + tangent_matvec, cell_material.cpp:170-194).
 inline void tangent_matvec(CellMaterials& cm, const Field9& f, const Field9& x, Field9& y) {

@@ -25,6 +25,8 @@ int main() {
   std::printf("{\"success\": %s, \"pbar\": [%.17g, %.17g, %.17g, %.17g], \"steps\": %zu, \"ls\": %lld}\n",
               r.report.success ? "true" : "false", r.pbar[0], r.pbar[1], r.pbar[3], r.pbar[4],
               r.report.steps.size(), (long long)r.report.ls_iterations);
+  // all-pure grid (factors 1): no laminate states to recover
+  if (!recover_composites(r.f, cm).empty()) return 3;
   try {
     SolverConfig bad = cfg;
     bad.eval = MaterialEval::dfmg;  // requires staggered (solver.cpp:277-280)
