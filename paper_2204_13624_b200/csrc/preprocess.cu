@@ -305,6 +305,30 @@ __device__ bool predicate(const GenArgs& g, double x, double y, double z) {
     }
     case 1:  // octahedron (:105-119)
       return fabs(wrapd(x - c0, g.L[0])) + fabs(wrapd(y - c1, g.L[1])) + fabs(wrapd(z - c2, g.L[2])) < g.p[0];
+    case 2: {  // fiber (image.cpp:123-155): p = axis, radius, length
+      const int axis = int(g.p[0]);
+      const double radius = g.p[1], hl = 0.5 * g.p[2];
+      double d[3] = {wrapd(x - c0, g.L[0]), wrapd(y - c1, g.L[1]), wrapd(z - c2, g.L[2])};
+      if (g.p[2] >= g.L[axis]) {
+        d[axis] = 0.0;
+      } else {
+        // capsule_dist with dir = e_axis: t = clamp(d . dir), q = d - t dir
+        const double t = fmin(fmax(d[axis], -hl), hl);
+        d[axis] = d[axis] - t;
+      }
+      return sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]) < radius;
+    }
+    case 3: {  // cross_ply (image.cpp:157-177): p = radius, pitch, layers
+      const double radius = g.p[0], pitch = g.p[1];
+      const int layers = int(g.p[2]);
+      const double lt = g.L[0] / layers;
+      const int ply = min(layers - 1, int(x / lt));
+      const double xc = (ply + 0.5) * lt;
+      const double dx = x - xc;
+      const double t = (ply % 2 == 0) ? z : y;
+      const double dt = wrapd(t - 0.5 * pitch, pitch);
+      return dx * dx + dt * dt < radius * radius;
+    }
     case 5: {  // slab (:214-227)
       const int axis = int(g.p[0]);
       const double l = g.L[axis];
@@ -553,8 +577,14 @@ int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double 
     const int64_t n = g.n1 * g.n2 * g.n3;
     DBuf<uint8_t> tmp;
     uint8_t* d = dev_or_stage(c, out, size_t(n), mem, tmp, false);
-    if (shape == 0 || shape == 1 || shape == 5) {
-      if (shape != 5 && g.p[0] < 0.0) throw ComboError(COMBO_ERR_BAD_SHAPE, "generate: radius must be >= 0");
+    if (shape == 0 || shape == 1 || shape == 2 || shape == 3 || shape == 5) {
+      if ((shape == 0 || shape == 1) && g.p[0] < 0.0)
+        throw ComboError(COMBO_ERR_BAD_SHAPE, "generate: radius must be >= 0");
+      if (shape == 2 && (g.p[0] < 0 || g.p[0] > 2)) throw ComboError(COMBO_ERR_BAD_SHAPE, "fiber: axis must be 0, 1, 2");
+      if (shape == 2 && g.p[1] < 0.0) throw ComboError(COMBO_ERR_BAD_SHAPE, "fiber: radius must be >= 0");
+      if (shape == 3 && g.p[2] < 1.0) throw ComboError(COMBO_ERR_BAD_SHAPE, "cross_ply: need at least one layer");
+      if (shape == 3 && (!(g.p[1] > 0.0) || g.p[0] < 0.0))
+        throw ComboError(COMBO_ERR_BAD_SHAPE, "cross_ply: pitch must be > 0 and radius >= 0");
       if (shape == 5 && (g.p[0] < 0 || g.p[0] > 2 || !(g.p[1] >= 0.0 && g.p[1] <= 1.0)))
         throw ComboError(COMBO_ERR_BAD_SHAPE, "slab: bad axis / fraction");
       k_generate<<<grid_for(n), 256, 0, c->stream>>>(g, d);
