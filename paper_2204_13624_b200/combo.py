@@ -310,7 +310,7 @@ class Context:
     def generate(self, shape, dims, lengths=(1.0, 1.0, 1.0), *params, out=None):
         """generate_* (image.cpp:57-227) and the seeded config generators;
         `out` may be a CUDA uint8 tensor (device result)."""
-        ids = {"sphere": 0, "octahedron": 1, "fiber": 2, "cross_ply": 3, "slab": 5, "rsa_spheres": 10, "rsa_fibers_z": 11,
+        ids = {"sphere": 0, "octahedron": 1, "fiber": 2, "cross_ply": 3, "fiber_pack": 4, "slab": 5, "rsa_spheres": 10, "rsa_fibers_z": 11,
                "boolean_ellipsoids": 12}
         if out is None:
             out = np.zeros(int(np.prod(dims)), dtype=np.uint8)

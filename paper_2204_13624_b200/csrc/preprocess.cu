@@ -353,6 +353,31 @@ __global__ void k_generate(GenArgs g, uint8_t* out) {
   }
 }
 
+// fiber_pack (image.cpp:179-212): every voxel centre against the capsule
+// list (centre, unit axis; generated on the host from the seed)
+__global__ void k_generate_pack(GenArgs g, const double* __restrict__ fib, int count, double hl, double radius,
+                                uint8_t* out) {
+  const int64_t n = g.n1 * g.n2 * g.n3;
+  for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = v % g.n3, j = (v / g.n3) % g.n2, i = v / (g.n2 * g.n3);
+    const double x[3] = {(double(i) + 0.5) * g.h[0], (double(j) + 0.5) * g.h[1], (double(k) + 0.5) * g.h[2]};
+    uint8_t in = 0;
+    for (int f = 0; f < count && !in; ++f) {
+      const double* c = fib + 6 * f;
+      const double* u = c + 3;
+      double d[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) d[a] = wrapd(x[a] - c[a], g.L[a]);
+      const double t = fmin(fmax(d[0] * u[0] + d[1] * u[1] + d[2] * u[2], -hl), hl);
+      double q[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) q[a] = d[a] - t * u[a];
+      in = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]) < radius;
+    }
+    out[v] = in;
+  }
+}
+
 // Object rasterization for the seeded config microstructures: one block per
 // object, threads sweep the (periodically wrapped) bounding box.
 struct Obj {
@@ -589,6 +614,32 @@ int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double 
         throw ComboError(COMBO_ERR_BAD_SHAPE, "slab: bad axis / fraction");
       k_generate<<<grid_for(n), 256, 0, c->stream>>>(g, d);
       ++c->launches;
+    } else if (shape == 4) {
+      // p = seed, count, radius, length, orientation_spread
+      const int count = int(g.p[1]);
+      const double radius = g.p[2], length = g.p[3], spread = g.p[4];
+      if (count < 0) throw ComboError(COMBO_ERR_BAD_SHAPE, "fiber_pack: count must be >= 0");
+      if (radius < 0.0 || length < 0.0) throw ComboError(COMBO_ERR_BAD_SHAPE, "fiber_pack: radius/length");
+      Sm64 rng{uint64_t(g.p[0])};
+      std::vector<double> fib(size_t(6) * size_t(std::max(count, 1)));
+      for (int f = 0; f < count; ++f) {
+        double* c = fib.data() + 6 * f;
+        c[0] = rng.unit() * g.L[0];
+        c[1] = rng.unit() * g.L[1];
+        c[2] = rng.unit() * g.L[2];
+        double d[3] = {1.0, 0.0, 0.0};
+        d[1] = spread * (2.0 * rng.unit() - 1.0);
+        d[2] = spread * (2.0 * rng.unit() - 1.0);
+        const double len = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        for (int a = 0; a < 3; ++a) c[3 + a] = d[a] / len;
+      }
+      DBuf<double> dfib;
+      dfib.alloc(fib.size());
+      COMBO_CK(cudaMemcpyAsync(dfib.p, fib.data(), fib.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      k_generate_pack<<<grid_for(n), 256, 0, c->stream>>>(g, dfib.p, count, 0.5 * length, radius, d);
+      ++c->launches;
+      COMBO_CK(cudaGetLastError());
+      COMBO_CK(cudaStreamSynchronize(c->stream));
     } else if (shape >= 10 && shape <= 12) {
       std::vector<Obj> objs;
       if (shape == 10) objs = rsa(g, uint64_t(g.p[0]), g.p[1], g.p[2], g.p[3], false);

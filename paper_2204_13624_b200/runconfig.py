@@ -15,8 +15,7 @@ runs on the device through the C-ABI: generation, coarsening and normals
 (`Context.generate/coarsen/compute_normals`), the solve and the phase
 averages and the per-composite laminate recovery behind the traction CSV
 (facet geometry is host arithmetic, facets.py). Out of scope: `bench` tables,
-the argv front end, and the fiber-pack generator (not on the device path;
-`generate` raises ConfigInvalid for it).
+and the argv front end.
 """
 from __future__ import annotations
 
@@ -308,6 +307,9 @@ def stage_generate(ctx, cfg):
         params = (float(int(g["axis"])), float(g["radius"]), float(g["length"]))
     elif shape == "cross_ply":
         params = (float(g["radius"]), float(g["pitch"]), float(int(g["layers"])))
+    elif shape == "fiber_pack":
+        params = (float(int(cfg.seed)), float(int(g["count"])), float(g["radius"]), float(g["length"]),
+                  float(g["orientation_spread"]))
     else:
         raise ConfigInvalid(f"generate: shape \"{shape}\" is not generated on the device path")
     img = cio.Image(ctx.generate(shape, tuple(cfg.dims), tuple(cfg.lengths), *params), cfg.lengths)

@@ -1,4 +1,4 @@
-"""Analytic device generators fiber / cross_ply (image.cpp:123-177) bit-exact
+"""Analytic device generators fiber / cross_ply / fiber_pack (image.cpp:123-212) bit-exact
 against the oracle (predicates at voxel centres, --fmad=false), including
 capsule ends, a full-length fiber, odd dims and non-unit lengths."""
 import numpy as np
@@ -12,6 +12,8 @@ CASES = [
     ("fiber", (16, 16, 16), (1.3, 1.0, 0.7), (1, 0.15, 0.3)),
     ("cross_ply", (24, 16, 20), (1.0, 1.0, 1.0), (0.08, 0.25, 4)),
     ("cross_ply", (19, 21, 13), (1.2, 0.8, 1.0), (0.1, 0.3, 3)),
+    ("fiber_pack", (24, 20, 16), (1.0, 0.9, 1.1), (7, 5, 0.08, 0.6, 0.3)),
+    ("fiber_pack", (12, 10, 8), (1.0, 0.9, 1.1), (3, 5, 0.1, 0.5, 0.2)),  # test_config.cpp:88-89
 ]
 
 
