@@ -48,3 +48,38 @@ def test_pipeline_stages(ctx, oracle, tmp_path):
     assert len(rows) - 1 == int(np.count_nonzero((g2.kind == 2) & (np.linalg.norm(g2.normal, axis=1) > 0)))
     for s in ("generate", "coarsen", "normals", "solve", "post"):
         assert (tmp_path / f"config_effective.{s}.json").exists()
+
+
+def test_cli_stage_chain(tmp_path):
+    """python -m paper_2204_13624_b200 generate/coarsen/normals/solve/post
+    (combo_main.cpp; test_cli.cpp:32-73): each stage exits 0, reports
+    reproduce modulo "timings"."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cfg = tmp_path / "cfg.json"
+    cfg.write_text(json.dumps({"geometry": {"shape": "sphere", "radius": 0.3}, "dims": [16, 16, 16],
+                               "coarsen": [2, 2, 2], "loading": [[1.0, 0.1, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]],
+                               "solver": {"scheme": "newton_cg", "tol_equilibrium": 1e-8},
+                               "output": {"dump_fields": True}}))
+    out = tmp_path / "o"
+
+    def run(stage):
+        r = subprocess.run([sys.executable, "-m", "paper_2204_13624_b200", stage, "--config", str(cfg), "--out",
+                            str(out)], cwd=root, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+
+    for s in ("generate", "coarsen", "normals", "solve"):
+        run(s)
+    rep1 = json.loads((out / "solve_report.json").read_text())
+    run("solve")
+    rep2 = json.loads((out / "solve_report.json").read_text())
+    strip = lambda j: {k: v for k, v in j["report"].items() if k != "timings"}  # noqa: E731
+    assert strip(rep1) == strip(rep2) and rep1["averages"] == rep2["averages"]
+    assert rep1["report"]["success"]
+    run("post")
+    assert (out / "averages.json").exists() and (out / "tractions.csv").exists()
+    assert json.loads((out / "coarsen_report.json").read_text())["volume_fraction_exact"]

@@ -80,3 +80,26 @@ def test_missing_upstream_artifacts(tmp_path):
     with pytest.raises(rc.UpstreamArtifactMissing):
         rc.stage_normals(None, c)
     assert (tmp_path / "o" / "config_effective.solve.json").exists()
+
+
+def test_cli_failures_exit_nonzero_with_json(tmp_path):
+    # test_cli.cpp:75-93
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    run = lambda *a: subprocess.run([sys.executable, "-m", "paper_2204_13624_b200", *a], cwd=root,  # noqa: E731
+                                    capture_output=True, text=True, timeout=120)
+    r = run("post", "--out", str(tmp_path / "o"))
+    assert r.returncode != 0
+    err = json.loads(r.stderr.strip().splitlines()[-1])
+    assert err["error"]["type"] == "UpstreamArtifactMissing" and err["error"]["message"]
+    bad = tmp_path / "bad.json"
+    bad.write_text(json.dumps({"bogus_key": 1}))
+    r = run("generate", "--config", str(bad))
+    assert r.returncode != 0
+    assert json.loads(r.stderr.strip().splitlines()[-1])["error"]["type"] == "ConfigInvalid"
+    r = run("solve", "--out", str(tmp_path / "o"), "--override", "solver.scheme=nope")
+    assert json.loads(r.stderr.strip().splitlines()[-1])["error"]["type"] == "ConfigInvalid"
