@@ -1,12 +1,12 @@
 """Staged command line (tools/combo_main.cpp:395-452) over the device path:
 
-  python -m paper_2204_13624_b200 {generate,coarsen,normals,solve,post}
+  python -m paper_2204_13624_b200 {generate,coarsen,normals,solve,post,bench}
       [--config cfg.json] [--out DIR] [--threads N] [--seed S] [--override key.path=value ...]
 
 Failures exit 1 with {"error": {"type": ..., "message": ...}} on stderr
 (test_cli.cpp:75-93). The device context is opened only when a stage first
 touches the GPU, so configuration and missing-artifact errors are reported
-without one. `bench` (desk-scale comparison tables) is not provided.
+without one. `bench --suite` writes the desk-scale comparison tables.
 """
 from __future__ import annotations
 
@@ -62,19 +62,24 @@ def load_config(a):
 def main(argv=None):
     ap = argparse.ArgumentParser(prog="python -m paper_2204_13624_b200")
     sub = ap.add_subparsers(dest="stage", required=True)
-    for name in ("generate", "coarsen", "normals", "solve", "post"):
+    for name in ("generate", "coarsen", "normals", "solve", "post", "bench"):
         p = sub.add_parser(name)
         p.add_argument("--config")
         p.add_argument("--out")
         p.add_argument("--threads", type=int)
         p.add_argument("--seed", type=int)
         p.add_argument("--override", action="append")
+        if name == "bench":
+            p.add_argument("--suite", default="sphere-smoke")
     a = ap.parse_args(argv)
     stages = {"generate": rc.stage_generate, "coarsen": rc.stage_coarsen, "normals": rc.stage_normals,
               "solve": rc.stage_solve, "post": rc.stage_post}
     try:
         cfg = load_config(a)
-        stages[a.stage](_LazyContext(), cfg)
+        if a.stage == "bench":
+            rc.stage_bench(_LazyContext(), cfg, a.suite)
+        else:
+            stages[a.stage](_LazyContext(), cfg)
     except Exception as e:  # noqa: BLE001 -- every failure becomes the JSON error record
         sys.stderr.write(json.dumps({"error": {"type": error_type(e), "message": str(e)}}) + "\n")
         return 1

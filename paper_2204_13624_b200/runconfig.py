@@ -408,3 +408,105 @@ def stage_post(ctx, cfg):
         cio.save_slice(f, dims, int(s.get("component", 1)), int(s.get("axis", 2)), int(s.get("index", 0)),
                        _artifact(cfg, f"slice_{n}.json"))
     return pa
+
+
+# ------------------------------------------------------------------- bench
+def _error_norm(p, ref):
+    """error_norm (postprocess.cpp:108-112)"""
+    d = float(np.linalg.norm(ref))
+    if not d > 0.0:
+        raise ValueError("error_norm: zero reference")
+    return float(np.linalg.norm(np.asarray(p) - np.asarray(ref))) / d
+
+
+def _bench_run(ctx, label, dims, kind, cp, nrm, combo, loading, scfg):
+    """bench_run (combo_main.cpp:277-293)"""
+    from .combo import CellMaterials, neo_hookean_enu
+
+    cm = CellMaterials(ctx, dims, kind, cp, nrm, neo_hookean_enu(1.0, 0.0), neo_hookean_enu(10.0, 0.3), combo=combo)
+    r = cm.solve(loading, scfg)
+    if not r["report"]["success"]:
+        raise RuntimeError("SolverFailed in bench: " + label)
+    pa = cm.phase_averages(r["f"])
+    z = np.zeros((3, 3))
+    return dict(label=label, pbar=pa["pbar"], pbar_plus=pa["pbar_plus"] if pa["has_plus"] else z,
+                pbar_minus=pa["pbar_minus"] if pa["has_minus"] else z,
+                seconds=float(r["report"].get("seconds_total", 0.0)))
+
+
+def _emit_table(rows, path):
+    """emit_table (combo_main.cpp:256-275): CSV against row 0 + console table"""
+    ref = rows[0]
+    with open(path, "w") as f:
+        f.write("label,XX,XY,YX,YY,err_pbar_pct,err_plus_pct,err_minus_pct,seconds\n")
+        g = lambda x: format(float(x), ".10g")  # noqa: E731
+        print("\n  label                          P_XX     P_XY     P_YX     P_YY   err%")
+        for r in rows:
+            e = _error_norm(r["pbar"], ref["pbar"]) * 100.0
+            ep = _error_norm(r["pbar_plus"], ref["pbar_plus"]) * 100.0
+            em = _error_norm(r["pbar_minus"], ref["pbar_minus"]) * 100.0
+            p = r["pbar"]
+            f.write(",".join([r["label"], g(p[0, 0]), g(p[0, 1]), g(p[1, 0]), g(p[1, 1]), g(e), g(ep), g(em),
+                              g(r["seconds"])]) + "\n")
+            print(f"  {r['label']:<28s} {p[0, 0]:8.4f} {p[0, 1]:8.4f} {p[1, 0]:8.4f} {p[1, 1]:8.4f} {e:6.3f}")
+        print()
+
+
+def stage_bench(ctx, cfg, suite="sphere-smoke"):
+    """cmd_bench (combo_main.cpp:295-393): desk-scale ComBo vs fine-grid
+    comparison tables (sphere-desk / sphere-smoke / octahedron-desk /
+    crossply-desk / fiber-desk), every solve on the device."""
+    from .combo import SolverConfig
+
+    _echo(cfg, "bench")
+    loading = np.eye(3)
+    loading[0, 1] = 0.5
+    scfg = SolverConfig(scheme="newton_cg", green="rotated", tol_equilibrium=1e-7, load_steps=2)
+    out = cfg.out_dir
+
+    def grid(img, fac, method="second_moment"):
+        kind, cp, _ = ctx.coarsen(img, fac)
+        dims = tuple(d // f for d, f in zip(img.shape, fac))
+        nrm = None
+        if method is not None:
+            nrm, _, _ = ctx.compute_normals(img, fac, kind, method=method)
+        return dims, kind, cp, nrm
+
+    def ref_row(img, label):
+        dims, kind, cp, _ = grid(img, (1, 1, 1), None)
+        return _bench_run(ctx, label, dims, kind, cp, np.zeros((kind.size, 3)), False, loading, scfg)
+
+    def combo_row(label, g, combo=True):
+        dims, kind, cp, nrm = g
+        return _bench_run(ctx, label, dims, kind, cp, nrm, combo, loading, scfg)
+
+    if suite in ("sphere-desk", "sphere-smoke"):
+        fine, tag = (128, "desk") if suite == "sphere-desk" else (64, "smoke")
+        img = ctx.generate("sphere", (fine,) * 3, (1.0, 1.0, 1.0), 0.4)
+        rows = [ref_row(img, f"ref {fine}^3 (no combo)")]
+        for fac in ((fine // 16,) * 3, (fine // 8, fine // 16, fine // 32)):
+            for method, m in (("barycenter", "barycenter"), ("second_moment", "second-moment")):
+                g = grid(img, fac, method)
+                res = "x".join(str(d) for d in g[0])
+                rows.append(combo_row(f"combo {res} {m}", g))
+        _emit_table(rows, os.path.join(out, f"bench_sphere_{tag}.csv"))
+    elif suite == "octahedron-desk":
+        img = ctx.generate("octahedron", (128,) * 3, (1.0, 1.0, 1.0), 0.4)
+        g = grid(img, (8, 8, 8))
+        rows = [ref_row(img, "ref 128^3 (no combo)"), combo_row("combo 16^3", g),
+                combo_row("staircase 16^3 (combo off)", g, combo=False)]
+        _emit_table(rows, os.path.join(out, "bench_octahedron.csv"))
+    elif suite == "crossply-desk":
+        img = ctx.generate("cross_ply", (100,) * 3, (1.0, 1.0, 1.0), 0.1, 0.25, 4)
+        rows = [ref_row(img, "ref 100^3 (no combo)"), combo_row("combo 25^3", grid(img, (4, 4, 4)))]
+        _emit_table(rows, os.path.join(out, "bench_crossply.csv"))
+    elif suite == "fiber-desk":
+        img = ctx.generate("fiber_pack", (126,) * 3, (1.0, 1.0, 1.0), float(cfg.seed), 30, 0.03, 0.5, 0.25)
+        rows = [ref_row(img, "ref 126^3 (no combo)")]
+        for fac in ((6, 6, 6), (9, 3, 3)):
+            g = grid(img, fac)
+            rows.append(combo_row("combo " + "x".join(str(d) for d in g[0]), g))
+        _emit_table(rows, os.path.join(out, "bench_fiber.csv"))
+    else:
+        raise ConfigInvalid(f"unknown bench suite \"{suite}\"")
+    return rows
