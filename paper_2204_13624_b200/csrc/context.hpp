@@ -104,19 +104,9 @@ struct FftPlan {
   // a power of two >= 8
   int rzL = 1, rzT = 32, rzLc = 1, rzTc = 32, ryW = 8, ryT = 32, rxW = 4, rxT = 32;
   size_t rzsmem = 0, rysmem = 0, rxsmem = 0;
-  // persistent double-buffered variants (fft_pp.cuh): buffer sizes (complex)
-  int pzbuf = 0, pybuf = 0, pxbuf = 0;
-  bool pipe_z = false, pipe_y = false, pipe_x = false;
-  int xv = 4;  // X+Gamma kernel variant (2 = xgamma_rr, 3 = xgamma_v3, 4 = rank-1 xgamma_v4)
   int xminb = 2;  // xgamma_v4 blocks per SM (launch bound)
-  int yminb = 2;  // y pass blocks per SM (launch bound)
-  bool fuse_zy = false;  // plane-pipelined Z/Y passes through L2 (COMBO_FUSE_ZY=0: five separate passes)
-  bool fuse_discard = true;
-  int fuse_wy = 0;  // y columns per fused tile (0: fill the z tile's threads)  // COMBO_FUSE_DISCARD=0: keep the consumed rows (write-back)
-  combo_host::DBuf<unsigned> sched;  // ticket + per-plane counters of the fused passes
   bool split_sweep = true;  // composite Newton pass + pure streaming pass (COMBO_SPLIT_SWEEP=0: one pass)
   bool mv_bulk = true;  // bulk-staged CG matvec (COMBO_MV_BULK=0: one cell per thread, direct loads)
-  bool y2 = false;  // y pass with two columns per thread (ypass_rr2)
   bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
   // slab decomposition (R ranks, this plan's rank q): planes [i0, i0 + ni)

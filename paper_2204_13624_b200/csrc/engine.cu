@@ -14,8 +14,6 @@
 #include <type_traits>
 
 #include "context.hpp"
-#include "fft_pp.cuh"
-#include "fft_fused.cuh"
 
 using namespace combo_dev;
 
@@ -191,23 +189,16 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->xW = W;
   p->xT = pick_threads(3 * d[0] * W);
   p->xsmem = size_t(3 * d[0] * W) * sizeof(double2);
-  // tuning knobs (benchmarks): COMBO_PIPE_{Z,Y,X}=1 selects the persistent
-  // cp.async pipelines, COMBO_ZLINES / COMBO_YW / COMBO_XW the tile shapes
+  // tuning knobs (benchmarks): COMBO_ZLINES / COMBO_YW / COMBO_XW the tile
+  // shapes, COMBO_XMINB the x+Gamma residency
   auto knob = [](const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
   };
-  p->pipe_z = knob("COMBO_PIPE_Z", 0) != 0;
-  p->pipe_y = knob("COMBO_PIPE_Y", 0) != 0;
-  p->pipe_x = knob("COMBO_PIPE_X", 0) != 0;
-  p->xv = knob("COMBO_XV", 4);
   p->xminb = knob("COMBO_XMINB", 2);
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
-  p->fuse_zy = knob("COMBO_FUSE_ZY", 0) != 0;  // experimental: see fft_fused.cuh
-  p->fuse_discard = knob("COMBO_FUSE_DISCARD", 1) != 0;
-  p->fuse_wy = knob("COMBO_FUSE_WY", 0);  // fused: 24.7 ms vs 15.5 + 5.7 split (512^3)
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
   if (n3 >= 8) {
     const int64_t tl = n3 / 8;
@@ -226,8 +217,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     p->rzLc = int(divisor_le(lines_for(384)));
     p->rzTc = int((((9 * p->rzLc + 1) / 2) * tl + 31) / 32 * 32);
     p->rzsmem = size_t(np * (n3 + n3 / 8)) * sizeof(double2);
-    const int64_t ls = n3 + n3 / 8, lsd = (ls + 1) & ~int64_t(1);
-    p->pzbuf = int(std::max({np * ls, (9 * Lz * lsd + 1) / 2, 9 * Lz * p->n3p}));
   }
   // j-major rows (single slab): x+Gamma 5.9 ms, y 4.05 / 4.09 ms; i-major: 6.8, 4.01 / 4.03 (512^3, round 1)
   p->swap = knob("COMBO_SWAP", 1) != 0;
@@ -241,7 +230,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     p->ryW = Wy;
     p->ryT = int(std::max<int64_t>(32, (Wy * (d[1] / 8) + 31) / 32 * 32));
     p->rysmem = size_t((d[1] + d[1] / 8) * Wy) * sizeof(double2);
-    p->pybuf = int((d[1] + d[1] / 8) * Wy);
   }
   if (d[0] >= 8) {
     int Wx = int(std::min<int64_t>(8, p->n3c));
@@ -249,15 +237,11 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     if (knob("COMBO_XW", 0) > 0) Wx = knob("COMBO_XW", 0);
     p->rxW = Wx;
     p->rxT = int(std::max<int64_t>(32, (Wx * (d[0] / 8) + 31) / 32 * 32));
-    p->rxsmem = size_t(3 * (d[0] + d[0] / 8) * Wx) * sizeof(double2);
-    p->pxbuf = int(3 * (d[0] + d[0] / 8) * Wx);
+    p->rxsmem = size_t(2 * (d[0] + d[0] / 8) * Wx) * sizeof(double2);
   }
   p->spec.alloc(size_t(9 * p->ni * d[1] * p->n3p));
   if (R > 1) {
     p->specB.alloc(size_t(9 * p->ni * d[1] * p->n3p));
-    // pipelined / older X variants are single-slab only
-    p->pipe_x = p->pipe_y = p->pipe_z = false;
-    p->xv = 4;
     p->swap = false;
   }
   c->plan = std::move(p);
@@ -432,21 +416,6 @@ void dispatch_log2(int64_t n, F&& f) {
   }
 }
 
-// persistent grid: resident blocks per SM x SMs, capped by the tile count
-template <class K>
-int pp_grid(const combo_ctx* c, K kernel, int threads, size_t smem, int64_t ntiles) {
-  int occ = 0;
-  COMBO_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
-  if (occ < 1) throw ComboError(COMBO_ERR_CUDA, "FFT pass does not fit on an SM");
-  return int(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(occ) * c->num_sms)));
-}
-
-bool pp_axis(int64_t n) {
-  for (int l = 3; l <= 10; ++l)
-    if (n == (int64_t(1) << l)) return true;
-  return false;
-}
-
 // CG matvec: bulk-staged persistent kernel (one CTA per SM) when the rows
 // are 16-byte aligned, else one cell per thread with direct loads.
 template <bool FIRST, bool HASX>
@@ -490,26 +459,12 @@ int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      const int64_t ntiles = (p.ni * p.dims[1] + p.rzL - 1) / p.rzL;
-      bool piped = false;
-      if constexpr (!Prod::CELL) {
-        if (p.pipe_z) {
-          const size_t smem = size_t(2 * p.pzbuf) * sizeof(double2);
-          auto k = zfwd_pp<Prod, L>;
-          smem_attr(k, smem);
-          nb = pp_grid(c, k, p.rzT, smem, ntiles);
-          k<<<unsigned(nb), p.rzT, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, ntiles, p.pzbuf, prod);
-          piped = true;
-        }
-      }
-      if (!piped) {
-        const int lz = Prod::CELL ? p.rzLc : p.rzL;
-        nb = (p.ni * p.dims[1] + lz - 1) / lz;
-        auto k = zfwd_rr<Prod, L>;
-        smem_attr(k, p.rzsmem);
-        k<<<unsigned(nb), Prod::CELL ? p.rzTc : p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, lz, prod,
-                                                                            nullptr);
-      }
+      const int lz = Prod::CELL ? p.rzLc : p.rzL;
+      nb = (p.ni * p.dims[1] + lz - 1) / lz;
+      auto k = zfwd_rr<Prod, L>;
+      smem_attr(k, p.rzsmem);
+      k<<<unsigned(nb), Prod::CELL ? p.rzTc : p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, lz, prod,
+                                                                          nullptr);
     } else {
       nb = (p.ni * p.dims[1] + p.zL - 1) / p.zL;
       double* part = Prod::NRED ? part_ptr(c, nb, Prod::NRED) : nullptr;
@@ -532,22 +487,11 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      const int64_t ntiles = (p.ni * p.dims[1] + p.rzL - 1) / p.rzL;
-      if (p.pipe_z) {
-        const size_t smem = size_t(2 * p.pzbuf) * sizeof(double2);
-        auto k = zinv_pp<Cons, L>;
-        smem_attr(k, smem);
-        nb = pp_grid(c, k, p.rzT, smem, ntiles);
-        double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
-        k<<<unsigned(nb), p.rzT, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, ntiles, p.pzbuf, scale, cons,
-                                                    part);
-      } else {
-        nb = ntiles;
-        double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
-        auto k = zinv_rr<Cons, L>;
-        smem_attr(k, p.rzsmem);
-        k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
-      }
+      nb = (p.ni * p.dims[1] + p.rzL - 1) / p.rzL;
+      double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
+      auto k = zinv_rr<Cons, L>;
+      smem_attr(k, p.rzsmem);
+      k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
     } else {
       nb = (p.ni * p.dims[1] + p.zL - 1) / p.zL;
       double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
@@ -568,31 +512,10 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
   dispatch_log2(p.dims[1], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      if (p.pipe_y) {
-        const int64_t ntiles = ((p.n3c + p.ryW - 1) / p.ryW) * p.ni * ncomp;
-        const size_t smem = size_t(2 * p.pybuf) * sizeof(double2);
-        auto k = ypass_pp<L, INV>;
-        smem_attr(k, smem);
-        const int g = pp_grid(c, k, p.ryT, smem, ntiles);
-        k<<<unsigned(g), p.ryT, smem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW, ntiles, p.pybuf);
-      } else {
-        dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.ni), unsigned(ncomp));
-        auto go = [&](auto k) {
-          smem_attr(k, p.rysmem);
-          k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
-        };
-        if (p.y2 && p.ryW >= 2 && p.ryW % 2 == 0 && p.ryW * (p.dims[1] / 8) / 2 <= 256) {
-          auto k = ypass_rr2<L, INV>;
-          smem_attr(k, p.rysmem);
-          k<<<grid, std::max(32, int(p.ryW * (p.dims[1] / 8) / 2 + 31) / 32 * 32), p.rysmem, c->stream>>>(
-              p.sv(), p.ax[1].tw.p, p.ryW);
-        } else if (p.yminb == 5 && p.ryT <= 256)
-          go(ypass_rr<L, INV, 256, 5>);
-        else if (p.yminb == 6 && p.ryT <= 256)
-          go(ypass_rr<L, INV, 256, 6>);
-        else
-          go(ypass_rr<L, INV>);
-      }
+      dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.ni), unsigned(ncomp));
+      auto k = ypass_rr<L, INV>;
+      smem_attr(k, p.rysmem);
+      k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
     } else {
       dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_kernel<L, INV>;
@@ -611,49 +534,26 @@ void launch_xgamma(combo_ctx* c, int kind) {
   dispatch_log2(p.dims[0], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      if (p.pipe_x) {
-        const int64_t ntiles = ((p.n3c + p.rxW - 1) / p.rxW) * p.nj * 3;
-        const size_t smem = size_t(2 * p.pxbuf) * sizeof(double2);
-        auto k = xgamma_pp<L>;
-        smem_attr(k, smem);
-        const int gr = pp_grid(c, k, p.rxT, smem, ntiles);
-        k<<<unsigned(gr), p.rxT, smem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g, ntiles, p.pxbuf);
-      } else {
-        dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), 3u);
-        if (p.xv == 4) {
-          const size_t smem = size_t(2 * (p.dims[0] + p.dims[0] / 8) * p.rxW) * sizeof(double2);
-          auto go = [&](auto k) {
-            smem_attr(k, smem);
-            k<<<grid, p.rxT, smem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
-          };
-          auto by_kind = [&](auto k0, auto k1, auto k2) {
-            if (kind == 0)
-              go(k0);
-            else if (kind == 1)
-              go(k1);
-            else
-              go(k2);
-          };
-          if (p.rxT > 256)
-            by_kind(xgamma_v4<L, 0, 512, 1>, xgamma_v4<L, 1, 512, 1>, xgamma_v4<L, 2, 512, 1>);
-          else if (p.xminb == 3)
-            by_kind(xgamma_v4<L, 0, 256, 3>, xgamma_v4<L, 1, 256, 3>, xgamma_v4<L, 2, 256, 3>);
-          else
-            by_kind(xgamma_v4<L, 0, 256, 2>, xgamma_v4<L, 1, 256, 2>, xgamma_v4<L, 2, 256, 2>);
-        } else if (p.xv == 3 && p.rxT <= 256) {
-          auto k = xgamma_v3<L, 256, 2>;
-          smem_attr(k, p.rxsmem);
-          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
-        } else if (p.xv == 3 || p.xv >= 5) {
-          auto k = xgamma_v3<L, 512, 1>;
-          smem_attr(k, p.rxsmem);
-          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
-        } else {
-          auto k = xgamma_rr<L>;
-          smem_attr(k, p.rxsmem);
-          k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
-        }
-      }
+      // rank-1 x + Gamma (fft_rr.cuh): two channels per thread
+      dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), 3u);
+      auto go = [&](auto k) {
+        smem_attr(k, p.rxsmem);
+        k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
+      };
+      auto by_kind = [&](auto k0, auto k1, auto k2) {
+        if (kind == 0)
+          go(k0);
+        else if (kind == 1)
+          go(k1);
+        else
+          go(k2);
+      };
+      if (p.rxT > 256)
+        by_kind(xgamma_v4<L, 0, 512, 1>, xgamma_v4<L, 1, 512, 1>, xgamma_v4<L, 2, 512, 1>);
+      else if (p.xminb == 3)
+        by_kind(xgamma_v4<L, 0, 256, 3>, xgamma_v4<L, 1, 256, 3>, xgamma_v4<L, 2, 256, 3>);
+      else
+        by_kind(xgamma_v4<L, 0, 256, 2>, xgamma_v4<L, 1, 256, 2>, xgamma_v4<L, 2, 256, 2>);
     } else {
       dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.nj), 3u);
       auto k = xgamma_kernel<L>;
@@ -687,98 +587,6 @@ void launch_x_plain(combo_ctx* c) {
   ++c->launches;
   COMBO_CK(cudaGetLastError());
 }
-// ---- plane-pipelined Z/Y passes (fft_fused.cuh)
-bool fuse_zy_ok(const combo_ctx* c) {
-  const FftPlan& p = *c->plan;
-#ifndef COMBO_WITH_FUSED_ZY
-  return false;
-#endif
-  return p.fuse_zy && !p.pipe_z && !p.pipe_y && pp_axis(p.dims[1]) && pp_axis(p.dims[2]) && p.rzL > 0;
-}
-
-struct FusedGeom {
-  int threads, wy;
-  size_t smem;
-};
-FusedGeom fused_geom(const FftPlan& p) {
-  const int tly = int(p.dims[1] / 8);
-  FusedGeom g;
-  g.wy = std::max(1, std::min<int>(8, p.rzT / tly));
-  if (p.fuse_wy > 0) g.wy = p.fuse_wy;
-  g.wy = int(std::min<int64_t>(g.wy, p.n3c));
-  g.threads = std::max(p.rzT, (g.wy * tly + 31) / 32 * 32);
-  g.smem = std::max(p.rzsmem, size_t((p.dims[1] + p.dims[1] / 8) * g.wy) * sizeof(double2));
-  return g;
-}
-
-combo_dev::PlaneSched plane_sched(combo_ctx* c, const FusedGeom& g) {
-  FftPlan& p = *c->plan;
-  p.sched.alloc(size_t(1 + p.ni));
-  COMBO_CK(cudaMemsetAsync(p.sched.p, 0, (1 + p.ni) * sizeof(unsigned), c->stream));
-  combo_dev::PlaneSched s;
-  s.ticket = p.sched.p;
-  s.done = p.sched.p + 1;
-  s.nplanes = p.ni;
-  s.zl = p.rzL;
-  s.nz = int(p.dims[1] / p.rzL);
-  s.wy = g.wy;
-  s.nyk = int((p.n3c + g.wy - 1) / g.wy);
-  s.discard = p.fuse_discard ? 1 : 0;
-  return s;
-}
-
-#ifdef COMBO_WITH_FUSED_ZY  // experimental, off by default (ptxas time; see fft_fused.cuh)
-template <class Prod>
-void launch_zy_fwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
-  FftPlan& p = *c->plan;
-  ProfScope ps(c, kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
-  const FusedGeom g = fused_geom(p);
-  const combo_dev::PlaneSched s = plane_sched(c, g);
-  dispatch_log2(p.dims[2], [&](auto Lz) {
-    constexpr int LZ = decltype(Lz)::value;
-    dispatch_log2(p.dims[1], [&](auto Ly) {
-      constexpr int LY = decltype(Ly)::value;
-      if constexpr (LZ >= 3 && LY >= 3) {
-        auto k = zy_fwd_fused<Prod, LZ, LY>;
-        smem_attr(k, g.smem);
-        const int64_t items = p.ni * (s.nz + 9 * s.nyk);
-        const int grid = pp_grid(c, k, g.threads, g.smem, items);
-        k<<<unsigned(grid), g.threads, g.smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.ax[1].tw.p, prod, s);
-      }
-    });
-  });
-  ++c->launches;
-  COMBO_CK(cudaGetLastError());
-}
-
-template <class Cons>
-int64_t launch_yz_inv(combo_ctx* c, const Cons& cons) {
-  FftPlan& p = *c->plan;
-  ProfScope ps(c, kTagZinv, spec_bytes(c) + 72.0 * double(c->N) * Cons::FIELDS);
-  const FusedGeom g = fused_geom(p);
-  const combo_dev::PlaneSched s = plane_sched(c, g);
-  const int64_t nb = p.ni * s.nz;  // z tiles = partial slots, as launch_zinv
-  double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
-  const double scale = 1.0 / double(c->Ng);
-  dispatch_log2(p.dims[2], [&](auto Lz) {
-    constexpr int LZ = decltype(Lz)::value;
-    dispatch_log2(p.dims[1], [&](auto Ly) {
-      constexpr int LY = decltype(Ly)::value;
-      if constexpr (LZ >= 3 && LY >= 3) {
-        auto k = yz_inv_fused<Cons, LZ, LY>;
-        smem_attr(k, g.smem);
-        const int64_t items = p.ni * (s.nz + 9 * s.nyk);
-        const int grid = pp_grid(c, k, g.threads, g.smem, items);
-        k<<<unsigned(grid), g.threads, g.smem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.ax[1].tw.p, scale, cons, part,
-                                                            s);
-      }
-    });
-  });
-  ++c->launches;
-  COMBO_CK(cudaGetLastError());
-  return nb;
-}
-#endif
 
 // Projection Pi(tau) = alpha Gamma^0 tau (green.cpp:133-151) with fused
 // producer / consumer, over every rank hosted by the leader c: prodf(k) /
@@ -792,33 +600,14 @@ void project_group(combo_ctx* c, int kind, PF&& prodf, CF&& consf, int slot_cons
   using Prod = std::decay_t<decltype(prodf(size_t(0)))>;
   using Cons = std::decay_t<decltype(consf(size_t(0)))>;
   static_assert(Prod::NRED == 0, "producer reductions are not combined across ranks");
-  const bool fz = !Prod::CELL && fuse_zy_ok(c);
-  for (size_t k = 0; k < ms.size(); ++k) {
-#ifdef COMBO_WITH_FUSED_ZY
-    if (fz) {
-      launch_zy_fwd(ms[k], prodf(k), prod_bytes);
-      continue;
-    }
-#endif
-    launch_zfwd(ms[k], prodf(k), prod_bytes);
-  }
-  if (!fz)
-    for (auto* m : ms) launch_y<false>(m);
+  for (size_t k = 0; k < ms.size(); ++k) launch_zfwd(ms[k], prodf(k), prod_bytes);
+  for (auto* m : ms) launch_y<false>(m);
   exchange(c, true);
   for (auto* m : ms) launch_xgamma(m, kind);
   exchange(c, false);
-  if (!fz)
-    for (auto* m : ms) launch_y<true>(m);
+  for (auto* m : ms) launch_y<true>(m);
   int64_t nbc = 0;
-  for (size_t k = 0; k < ms.size(); ++k) {
-#ifdef COMBO_WITH_FUSED_ZY
-    if (fz) {
-      nbc = launch_yz_inv(ms[k], consf(k));
-      continue;
-    }
-#endif
-    nbc = launch_zinv(ms[k], consf(k));
-  }
+  for (size_t k = 0; k < ms.size(); ++k) nbc = launch_zinv(ms[k], consf(k));
   if (Cons::NRED) group_reduce(c, nbc, Cons::NRED, slot_cons);
 }
 

@@ -438,218 +438,7 @@ static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const
   ypass_tile<L, INV>(sv, tw, W, blockIdx.z, blockIdx.y, blockIdx.x * W);
 }
 
-// Y pass with two columns per thread (columns line and line + W/2): twice the
-// independent loads per thread at the same warp count, so W = 8 tiles (128-
-// byte row segments) run with 256 threads.
-template <int L, bool INV>
-static __global__ void __launch_bounds__(256, 2) ypass_rr2(SpecView sv, const double2* __restrict__ tw, int W) {
-  constexpr int N = 1 << L;
-  extern __shared__ double2 sm[];
-  const int W2 = W >> 1;
-  const int c = blockIdx.z, i = blockIdx.y, kc0 = blockIdx.x * W;
-  const int w = min(W, int(sv.n3c) - kc0);
-  const int line = threadIdx.x % W2, u = threadIdx.x / W2;
-  const bool active = u < N / 8;
-  const bool on[2] = {line < w, line + W2 < w};
-  double2* base = sv.spec + int64_t(c) * sv.cs + kc0 + line;
-  double2 v[2][8];
-  if (active) {
-#pragma unroll
-    for (int ch = 0; ch < 2; ++ch)
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        v[ch][q] = on[ch] ? base[sv.rowA(i, rr_first_pos<L, false>(u, q)) + ch * W2] : make_double2(0.0, 0.0);
-  }
-  auto addr = [&](int ch, int pos) { return pad8(pos) * W + ch * W2 + line; };
-  rr_stages<L, INV, false, 0, 2>(v, u, active, sm, tw, addr);
-  if (active) {
-#pragma unroll
-    for (int ch = 0; ch < 2; ++ch)
-      if (on[ch]) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) base[sv.rowA(i, rr_final_pos<L, false>(u, q)) + ch * W2] = v[ch][q];
-      }
-  }
-}
-
 // ---------------------------------------------------------------- X + Gamma
-// W columns per block, 3 components (row group) per thread.
-template <int L>
-static __global__ void __launch_bounds__(256, 2)
-    xgamma_rr(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G) {
-  constexpr int N = 1 << L;
-  extern __shared__ double2 sm[];
-  const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
-  const int w = min(W, int(sv.n3c) - kc0);
-  const int line = threadIdx.x % W, u = threadIdx.x / W;
-  const bool active = line < w && u < N / 8;
-  const int64_t plane = sv.cs;
-  double2* base = sv.spec + int64_t(3 * rg) * plane + kc0 + line;  // pencil side, local k2 j
-  double2 v[3][8];
-  if (active) {
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[ch][q] = base[int64_t(ch) * plane + sv.rowB(rr_first_pos<L, false>(u, q), j)];
-  }
-  const int chs = (N + N / 8) * W;  // channel stride in smem
-  auto addr = [&](int ch, int pos) { return ch * chs + pad8(pos) * W + line; };
-  rr_stages<L, false, false, 0, 3>(v, u, active, sm, tw, addr);
-  if (active) {
-    const int64_t k3 = kc0 + line;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int64_t k1 = rr_final_pos<L, false>(u, q);
-      double2 t[3] = {v[0][q], v[1][q], v[2][q]};
-      gamma_row(G, rg, k1, sv.j0 + j, k3, sv.n1, sv.n2, sv.n3, t);
-      v[0][q] = t[0];
-      v[1][q] = t[1];
-      v[2][q] = t[2];
-    }
-  }
-  // the reversed radix order's first stage consumes these registers as-is
-  rr_stages<L, true, true, 0, 3>(v, u, active, sm, tw, addr);
-  if (active) {
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) base[int64_t(ch) * plane + sv.rowB(rr_final_pos<L, true>(u, q), j)] = v[ch][q];
-  }
-}
-
-// Gamma with the per-column factors hoisted out of the k1 loop: a thread's
-// column (k2, k3) is fixed, so the rotated symbol g = (f1 a2 a3, f2 a1 a3,
-// f3 a1 a2) costs three complex products per k-point, and the 1/den scaling
-// one reciprocal (green.cpp:67-130 up to the rounding of the factor order).
-struct GammaCol {
-  double2 c0, c1, c2;  // per-column factors of g0, g1, g2
-  double d12;          // continuous: xi1^2 + xi2^2
-  bool nyq;            // continuous: an axis of the column is at Nyquist
-};
-
-__device__ __forceinline__ GammaCol gamma_col(const GreenTables& G, int64_t k2, int64_t k3, int64_t n2,
-                                              int64_t n3) {
-  GammaCol c;
-  if (G.kind == 0) {
-    c.c1 = make_double2(0.0, G.xi[1][k2]);
-    c.c2 = make_double2(0.0, G.xi[2][k3]);
-    c.d12 = c.c1.y * c.c1.y + c.c2.y * c.c2.y;
-    c.nyq = 2 * k2 == n2 || 2 * k3 == n3;
-    c.c0 = make_double2(0.0, 0.0);
-  } else if (G.kind == 1) {
-    const double2 a2 = G.avg[1][k2], a3 = G.avg[2][k3];
-    c.c0 = cmul(a2, a3);
-    c.c1 = cmul(G.fwd[1][k2], a3);
-    c.c2 = cmul(G.fwd[2][k3], a2);
-    c.d12 = 0.0;
-    c.nyq = false;
-  } else {
-    c.c1 = G.fwd[1][k2];
-    c.c2 = G.fwd[2][k3];
-    c.c0 = make_double2(0.0, 0.0);
-    c.d12 = 0.0;
-    c.nyq = false;
-  }
-  return c;
-}
-
-__device__ __forceinline__ void gamma_row_col(const GreenTables& G, const GammaCol& c, int row, int64_t k1,
-                                              int64_t n1, double2* t) {
-  if (G.kind == 0) {
-    if (c.nyq || 2 * k1 == n1) {
-      t[0] = t[1] = t[2] = make_double2(0.0, 0.0);
-      return;
-    }
-    const double x0 = G.xi[0][k1];
-    const double den = x0 * x0 + c.d12;
-    if (den == 0.0) {
-      t[0] = t[1] = t[2] = make_double2(0.0, 0.0);
-      return;
-    }
-    // g = i xi: tau_J = xi_J (sum_L xi_L tau_L) / den
-    const double sx = x0 * t[0].x + c.c1.y * t[1].x + c.c2.y * t[2].x;
-    const double sy = x0 * t[0].y + c.c1.y * t[1].y + c.c2.y * t[2].y;
-    const double r = 1.0 / den;
-    const double x[3] = {x0 * r, c.c1.y * r, c.c2.y * r};
-#pragma unroll
-    for (int J = 0; J < 3; ++J) t[J] = make_double2(x[J] * sx, x[J] * sy);
-    return;
-  }
-  double2 g[3];
-  if (G.kind == 1) {
-    const double2 a1 = G.avg[0][k1];
-    g[0] = cmul(G.fwd[0][k1], c.c0);
-    g[1] = cmul(c.c1, a1);
-    g[2] = cmul(c.c2, a1);
-  } else {
-    g[0] = G.fwd[0][k1];
-    g[1] = c.c1;
-    g[2] = c.c2;
-  }
-  const double den = (g[0].x * g[0].x + g[0].y * g[0].y) + (g[1].x * g[1].x + g[1].y * g[1].y) +
-                     (g[2].x * g[2].x + g[2].y * g[2].y);
-  if (den == 0.0) {
-    t[0] = t[1] = t[2] = make_double2(0.0, 0.0);
-    return;
-  }
-  double2 gr[3];
-#pragma unroll
-  for (int J = 0; J < 3; ++J) gr[J] = (G.kind == 2 && J != row) ? make_double2(-g[J].x, g[J].y) : g[J];
-  double sx = 0.0, sy = 0.0;
-#pragma unroll
-  for (int L = 0; L < 3; ++L) {
-    sx += gr[L].x * t[L].x + gr[L].y * t[L].y;
-    sy += gr[L].x * t[L].y - gr[L].y * t[L].x;
-  }
-  const double r = 1.0 / den;
-  const double2 s = make_double2(sx * r, sy * r);
-#pragma unroll
-  for (int J = 0; J < 3; ++J) t[J] = cmul(gr[J], s);
-}
-
-// X + Gamma, variant 3: column-hoisted Gamma; MAXT = launch bound (256 with
-// 2 blocks/SM, or 512 with W = 8 and 1 block/SM).
-template <int L, int MAXT, int MINB>
-static __global__ void __launch_bounds__(MAXT, MINB)
-    xgamma_v3(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G) {
-  constexpr int N = 1 << L;
-  extern __shared__ double2 sm[];
-  const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
-  const int w = min(W, int(sv.n3c) - kc0);
-  const int line = threadIdx.x % W, u = threadIdx.x / W;
-  const bool active = line < w && u < N / 8;
-  const int64_t plane = sv.cs;
-  double2* base = sv.spec + int64_t(3 * rg) * plane + kc0 + line;  // pencil side, local k2 j
-  double2 v[3][8];
-  if (active) {
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[ch][q] = base[int64_t(ch) * plane + sv.rowB(rr_first_pos<L, false>(u, q), j)];
-  }
-  const int chs = (N + N / 8) * W;
-  auto addr = [&](int ch, int pos) { return ch * chs + pad8(pos) * W + line; };
-  rr_stages<L, false, false, 0, 3>(v, u, active, sm, tw, addr);
-  if (active) {
-    const GammaCol col = gamma_col(G, sv.j0 + j, kc0 + line, sv.n2, sv.n3);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      double2 t[3] = {v[0][q], v[1][q], v[2][q]};
-      gamma_row_col(G, col, rg, rr_final_pos<L, false>(u, q), sv.n1, t);
-      v[0][q] = t[0];
-      v[1][q] = t[1];
-      v[2][q] = t[2];
-    }
-  }
-  rr_stages<L, true, true, 0, 3>(v, u, active, sm, tw, addr);
-  if (active) {
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) base[int64_t(ch) * plane + sv.rowB(rr_final_pos<L, true>(u, q), j)] = v[ch][q];
-  }
-}
-
 // ------------------------------------------------ X + Gamma, rank-1 variant
 // Gamma^0 row rg at k is rank one: tau_J <- gr_J s / den with
 // s = sum_L conj(gr_L) tau_L (green.cpp:67-130). In all three schemes the

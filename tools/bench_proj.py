@@ -1,6 +1,6 @@
 """Projection-only microbenchmark: combo_project on a random 9-component
 field resident on the device; per-pass CUDA-event times from the library
-profiler. Tuning knobs are read from the environment (COMBO_PIPE_*, COMBO_*W,
+profiler. Tuning knobs are read from the environment (COMBO_XW, COMBO_YW,
 COMBO_ZLINES). Usage: python tools/bench_proj.py N [reps]"""
 import ctypes as C
 import json
