@@ -297,15 +297,16 @@ class CellMaterials:
         return y
 
     def solve(self, fbar, scheme=1, green=1, eval=0, tol=1e-8, max_outer=200, cg_tol=1e-2, cg_max=2000,
-              load_steps=1, max_bisections=5, max_ls_iterations=0, want_fields=True):
+              load_steps=1, max_bisections=5, max_ls_iterations=0, want_fields=True, want_p=None):
         cfg = SolverCfg(scheme, green, eval, tol, max_outer, cg_tol, cg_max, load_steps, max_bisections,
                         0, 0, max_ls_iterations)
+        want_p = want_fields if want_p is None else want_p
         F = np.zeros(9 * self.n) if want_fields else None
-        P = np.zeros(9 * self.n) if want_fields else None
+        P = np.zeros(9 * self.n) if want_p else None
         pbar = np.zeros(9)
         ptr = lib().oracle_solve(self._h, _f64(np.asarray(fbar).ravel()), C.byref(cfg),
                                  F.ctypes.data_as(C.c_void_p) if want_fields else None,
-                                 P.ctypes.data_as(C.c_void_p) if want_fields else None, pbar)
+                                 P.ctypes.data_as(C.c_void_p) if want_p else None, pbar)
         rep = json.loads(C.string_at(ptr).decode())
         lib().oracle_free(ptr)
         return dict(f=F, p=P, pbar=pbar.reshape(3, 3), report=rep)

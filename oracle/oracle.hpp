@@ -365,7 +365,9 @@ struct SweepStats {  // cell_material.hpp:76-84
   int laminate_iter_max = 0;
 };
 SweepStats stress_sweep(CellMaterials& cm, const Field9& f, Field9& p,
-                        std::vector<double>* tangents45);
+                        std::vector<double>* tangents45, bool lean = false);
+void tangent_matvec_lean(const CellMaterials& cm, const std::vector<double>& t45c, const Field9& f,
+                         const Field9& x, Field9& y);
 void tangent_matvec(const std::vector<double>& t45, const Field9& x, Field9& y);
 void pack45(const Mat9& a, double* dst);
 Mat9 unpack45(const double* src);

@@ -435,11 +435,14 @@ Mat9 unpack45(const double* src) {
   return a;
 }
 
-// cell_material.cpp:104-168
-SweepStats stress_sweep(CellMaterials& cm, const Field9& f, Field9& p, std::vector<double>* t45) {
+// cell_material.cpp:104-168. lean: t45 holds the composite cells' tangents
+// only (by combo id); pure cells' tangents are recomputed from F by
+// tangent_matvec_lean (same arithmetic, 360 B/cell less: the 512^3 fixture
+// and CPU baseline fit the B200 box's host RAM).
+SweepStats stress_sweep(CellMaterials& cm, const Field9& f, Field9& p, std::vector<double>* t45, bool lean) {
   const std::int64_t n = cm.cells();
   if (p.cells() != n) p = Field9(f.grid);
-  if (t45) t45->resize(std::size_t(45 * n));
+  if (t45) t45->resize(std::size_t(45 * (lean ? std::max<std::int64_t>(cm.composite_cells(), 1) : n)));
   std::atomic<std::int64_t> inadmissible{0}, failures{0}, backproj{0};
   std::atomic<int> iter_max{0};
   const bool want_tan = t45 != nullptr;
@@ -459,7 +462,7 @@ SweepStats stress_sweep(CellMaterials& cm, const Field9& f, Field9& p, std::vect
       } catch (const InadmissibleMacroState&) {
         inadmissible.fetch_add(1, std::memory_order_relaxed);
         p.set_cell(si, Mat3());
-        if (want_tan) pack45(Mat9::identity(), t45->data() + 45 * i);
+        if (want_tan) pack45(Mat9::identity(), t45->data() + 45 * (lean ? std::int64_t(id) : i));
         continue;
       }
       if (!sol.state.converged) failures.fetch_add(1, std::memory_order_relaxed);
@@ -471,6 +474,11 @@ SweepStats stress_sweep(CellMaterials& cm, const Field9& f, Field9& p, std::vect
       cm.warm_all()[std::size_t(id)] = sol.state.a;
       pc = sol.result.p_box;
       if (want_tan) ac = sol.result.a_box;
+      if (want_tan && lean) {
+        pack45(ac, t45->data() + 45 * std::int64_t(id));
+        p.set_cell(si, pc);
+        continue;
+      }
     } else {
       const Law& law = ph == 1 ? cm.inclusion() : cm.matrix();
       const bool ok = want_tan ? law_eval_tangent(law, fc, pc, ac) : law_eval(law, fc, pc);
@@ -481,7 +489,7 @@ SweepStats stress_sweep(CellMaterials& cm, const Field9& f, Field9& p, std::vect
       }
     }
     p.set_cell(si, pc);
-    if (want_tan) pack45(ac, t45->data() + 45 * i);
+    if (want_tan && !lean) pack45(ac, t45->data() + 45 * i);
   }
   SweepStats st;
   st.inadmissible_cells = inadmissible.load();
@@ -511,6 +519,44 @@ void tangent_matvec(const std::vector<double>& t45, const Field9& x, Field9& y) 
       }
     }
     for (int c = 0; c < 9; ++c) y.data[std::size_t(c) * std::size_t(n) + std::size_t(i)] = yv[c];
+  }
+}
+
+// tangent_matvec with the lean tangent storage of stress_sweep: composite
+// tangents by combo id, pure cells' tangents re-evaluated at F (identical
+// to the stored ones: same law, same F, same pack45 symmetrization)
+void tangent_matvec_lean(const CellMaterials& cm, const std::vector<double>& t45c, const Field9& f,
+                         const Field9& x, Field9& y) {
+  const std::int64_t n = x.cells();
+  if (y.cells() != n) y = Field9(x.grid);
+#pragma omp parallel for schedule(static)
+  for (std::int64_t i = 0; i < n; ++i) {
+    const auto si = std::size_t(i);
+    double own[45];
+    const double* a = own;
+    const std::uint8_t ph = cm.cell_phase(si);
+    if (ph == 2) {
+      a = t45c.data() + 45 * std::int64_t(cm.combo_id(si));
+    } else {
+      const Law& law = ph == 1 ? cm.inclusion() : cm.matrix();
+      Mat3 pc;
+      Mat9 ac;
+      if (!law_eval_tangent(law, f.cell(si), pc, ac)) ac = Mat9::identity();
+      pack45(ac, own);
+    }
+    double xv[9], yv[9];
+    for (int c = 0; c < 9; ++c) xv[c] = x.data[std::size_t(c) * std::size_t(n) + si];
+    for (int c = 0; c < 9; ++c) yv[c] = 0.0;
+    int t = 0;
+    for (int r = 0; r < 9; ++r) {
+      yv[r] += a[t] * xv[r];
+      ++t;
+      for (int c = r + 1; c < 9; ++c, ++t) {
+        yv[r] += a[t] * xv[c];
+        yv[c] += a[t] * xv[r];
+      }
+    }
+    for (int c = 0; c < 9; ++c) y.data[std::size_t(c) * std::size_t(n) + si] = yv[c];
   }
 }
 
@@ -768,6 +814,8 @@ class CellSolver {
     cm_.spectrum_bounds(Mat3::identity(), lo, hi);
     stress_floor_ = 1e-12 * std::max(hi, 1e-12);
     if (cfg_.eval == kDfmg) dfmg_state_.resize(grid_.cells());
+    const char* lean = std::getenv("ORACLE_LEAN_TANGENTS");
+    lean_ = lean && std::atoi(lean) != 0 && cfg_.eval != kDfmg;
   }
   StepReport run_step(Field9& f, const Mat3& fbar, double t0, double t1);
   const Field9& stress() const { return p_; }
@@ -775,6 +823,7 @@ class CellSolver {
   double alpha() const { return alpha_; }
   DfmgState& dfmg_state() { return dfmg_state_; }
   std::int64_t ls_total = 0;
+  StepReport partial;  // the step cut short by the LS budget
 
  private:
   void project(const Field9& in, Field9& out) {
@@ -795,11 +844,14 @@ class CellSolver {
       s2.back_projections = s1.back_projections;
       return s2;
     }
-    return stress_sweep(cm_, f, p_, &tangents_);
+    tan_f_ = &f;
+    return stress_sweep(cm_, f, p_, &tangents_, lean_);
   }
   void apply_tangent(const Field9& x, Field9& y) {
     if (cfg_.eval == kDfmg)
       dfmg_tangent_matvec(tangents_, x, y);
+    else if (lean_)
+      tangent_matvec_lean(cm_, tangents_, *tan_f_, x, y);
     else
       tangent_matvec(tangents_, x, y);
   }
@@ -825,6 +877,8 @@ class CellSolver {
   Fft3 fft_;
   Field9 p_, proj_;
   std::vector<double> tangents_;
+  bool lean_ = false;             // ORACLE_LEAN_TANGENTS=1 (see stress_sweep)
+  const Field9* tan_f_ = nullptr;  // F of the tangents (lean matvec)
   DfmgState dfmg_state_;
   Mat3 pbar_;
   double alpha_ = 1.0;
@@ -973,7 +1027,10 @@ StepReport CellSolver::run_step(Field9& f, const Mat3& fbar, double t0, double t
   try {
     ok = cfg_.scheme == kBasic ? run_basic(f, fbar, rep) : run_newton(f, fbar, rep);
   } catch (const LsBudgetExhausted&) {
+    // the partial step is reported (parity of budgeted runs, not reference
+    // behaviour: the reference has no LS budget)
     rep.seconds = seconds_since(tic);
+    partial = std::move(rep);
     throw;
   }
   rep.converged = ok;
@@ -1030,6 +1087,7 @@ SolveResult solve(CellMaterials& cm, const Mat3& fbar_target, const SolverConfig
       dt = 0.5 * dt_try;
     }
   } catch (const LsBudgetExhausted&) {
+    report.steps.push_back(std::move(solver.partial));
     report.success = false;
     report.error = "LsBudgetExhausted";
   }

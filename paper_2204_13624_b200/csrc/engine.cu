@@ -1258,7 +1258,15 @@ void Solver::run(const double* fbar_target, combo_report& report) {
       rep.t_end = t + dt_try;
       std::memcpy(rep.fbar, fbar, sizeof fbar);
       const auto st0 = Clock::now();
-      const bool ok = run_step(fbar, rep);
+      bool ok = false;
+      try {
+        ok = run_step(fbar, rep);
+      } catch (const LsBudget&) {
+        // the step cut short by the LS budget is reported (oracle/solver.cpp)
+        rep.seconds = since(st0);
+        report.steps.push_back(std::move(rep));
+        throw;
+      }
       rep.converged = ok;
       rep.seconds = since(st0);
       if (ok) {
@@ -1266,6 +1274,12 @@ void Solver::run(const double* fbar_target, combo_report& report) {
         t += dt_try;
         std::memcpy(fbar_prev, fbar, sizeof fbar);
         continue;
+      }
+      // P of the solve is the stress of the last evaluated F (solver.cpp:343,
+      // p_): keep that F out of the slot the backup is restored into
+      if (last_eval_ == F_) {
+        copy_all(Fo_, F_);
+        last_eval_ = Fo_;
       }
       save_or_restore(false);
       shF_ = zero_shift();

@@ -1,0 +1,66 @@
+"""Full-size parity cases (BASELINE.json configs C2-C5 at their real sizes)
+shared by the fixture generator (tools/fullsize_fixtures.py, CPU oracle) and
+the GPU test (tests/test_gpu_fullsize.py).
+
+A case is a config of paper_2204_13624_b200/configs.py solved along the
+reference's load path (/root/reference/proj/src/solver.cpp:286-346) with an
+optional LS-iteration budget (C4 and C5: the oracle needs hours for the full
+paths at 256^3 DFMG / 512^3). The fixture stores what the GPU run is checked
+against: digests of the preprocessing outputs (bit-exact), the whole report
+(per-step and per-iteration P-bar and residual histories, Newton / CG / line
+search counts), per-component sums of F and F itself at seeded sample cells.
+"""
+import hashlib
+
+import numpy as np
+
+# case -> config, whether the path is the config's first load increment
+# only (as a single step; else the config's whole ramp) and the LS budget
+# (0: unlimited)
+CASES = {
+    "C2": dict(config="C2", first_increment=False, max_ls=0),
+    "C3": dict(config="C3", first_increment=False, max_ls=0),
+    "C4": dict(config="C4", first_increment=False, max_ls=70),
+    # the bench workload itself (bench.py: C5 1-GPU variant, first increment)
+    "C5": dict(config="C5", first_increment=True, max_ls=0),
+}
+
+N_SAMPLE = 1024  # uniform sample cells (+ as many composite cells)
+
+
+def case_fbar(cfg, case):
+    if case["first_increment"]:
+        return np.eye(3) + (cfg.fbar - np.eye(3)) / cfg.load_steps, 1
+    return cfg.fbar, cfg.load_steps
+
+
+def digest(a):
+    """sha256 of the raw little-endian bytes of an array (host or CUDA)."""
+    if hasattr(a, "is_cuda"):
+        a = a.cpu().numpy()
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.view(np.uint8).ravel().data).hexdigest()
+
+
+def grid_digests(kind, c_plus, count, normals, flags):
+    return {"kind": digest(kind), "c_plus": digest(c_plus), "count": digest(count), "normals": digest(normals),
+            "flags": digest(flags)}
+
+
+def sample_cells(kind, seed=20260):
+    """Seeded uniform cells plus seeded composite cells (kind 2), sorted."""
+    kind = np.asarray(kind).ravel()
+    rng = np.random.default_rng(seed)
+    uni = rng.choice(kind.size, size=min(N_SAMPLE, kind.size), replace=False)
+    comp = np.flatnonzero(kind == 2)
+    if comp.size:
+        comp = rng.choice(comp, size=min(N_SAMPLE, comp.size), replace=False)
+    return np.unique(np.concatenate([uni, comp])).astype(np.int64)
+
+
+def field_summary(F, n, cells):
+    """per-component sums / sums of squares (float64, numpy pairwise) and the
+    9 components at the sample cells of a [9][n] field."""
+    F = np.asarray(F).reshape(9, n)
+    return {"sum": F.sum(axis=1).tolist(), "sumsq": np.einsum("ij,ij->i", F, F).tolist(),
+            "sumabs": np.abs(F).sum(axis=1).tolist()}, F[:, cells].T.copy()

@@ -289,3 +289,24 @@ def test_phase_averages_all_matrix(oracle):
     pa = cm.phase_averages(r["f"])
     assert not pa["has_plus"] and pa["has_minus"]
     assert np.linalg.norm(pa["pbar_minus"] - pa["pbar"]) <= 1e-14 * np.linalg.norm(pa["pbar"])
+
+
+def test_lean_tangent_storage_bitwise(oracle, monkeypatch):
+    """ORACLE_LEAN_TANGENTS=1 (composite tangents only, pure cells re-evaluated
+    in the matvec; used for the 512^3 fixtures and CPU baseline) gives the
+    same solve bit for bit, including a budget-cut partial step."""
+    img = oracle.generate("rsa_spheres", (64, 64, 64), (1, 1, 1), 1, 2.0, 6.0, 0.3)
+    kind, cp, _ = oracle.coarsen(img, (4, 4, 4))
+    nrm, _, _ = oracle.normals(img, (4, 4, 4))
+    fbar = np.eye(3)
+    fbar[0, 0] += 0.02
+    out = []
+    for lean in ("0", "1"):
+        monkeypatch.setenv("ORACLE_LEAN_TANGENTS", lean)
+        cm = oracle.CellMaterials((16, 16, 16), kind, cp, nrm, oracle.neo_hookean(2.0, 1.0),
+                                  oracle.neo_hookean(200.0, 100.0))
+        out.append(cm.solve(fbar, scheme=1, green=1, tol=1e-8, load_steps=1, max_ls_iterations=30))
+    a, b = out
+    assert a["report"]["error"] == "LsBudgetExhausted" and len(a["report"]["steps"]) == 1
+    assert a["report"]["steps"][0]["residuals"] == b["report"]["steps"][0]["residuals"]
+    assert np.array_equal(a["f"].view(np.uint64), b["f"].view(np.uint64))
