@@ -19,7 +19,9 @@ import argparse
 import json
 import os
 import platform
+import resource
 import sys
+import threading
 import time
 
 import numpy as np
@@ -43,6 +45,23 @@ def cpu_model():
     except OSError:
         pass
     return platform.processor()
+
+
+def mem_guard(min_avail_gb=10.0):
+    """exit before the host runs out of memory (the box must survive)"""
+    def watch():
+        while True:
+            try:
+                for line in open("/proc/meminfo"):
+                    if line.startswith("MemAvailable:"):
+                        if int(line.split()[1]) / 2**20 < min_avail_gb:
+                            print("mem_guard: MemAvailable below %.0f GB, aborting" % min_avail_gb, flush=True)
+                            os._exit(3)
+            except OSError:
+                return
+            time.sleep(0.5)
+
+    threading.Thread(target=watch, daemon=True).start()
 
 
 def run_case(name, out_dir):
@@ -81,7 +100,8 @@ def run_case(name, out_dir):
         "report": rep, "pbar": r["pbar"].ravel().tolist(), "f_sums": sums, "sample_cells": cells.tolist(),
         "cpu": {"cores": os.cpu_count(), "model": cpu_model(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS"),
                 "preprocess_s": t_pre, "solve_s": t_solve,
-                "boxel_iterations_per_s": n * rep["ls_total"] / t_solve if t_solve > 0 else None},
+                "boxel_iterations_per_s": n * rep["ls_total"] / t_solve if t_solve > 0 else None,
+                "peak_rss_gb": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20},
         "generator": "tools/fullsize_fixtures.py (CPU oracle)",
     }
     os.makedirs(out_dir, exist_ok=True)
@@ -96,6 +116,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden"))
     a = ap.parse_args()
     os.environ.setdefault("OMP_PROC_BIND", "close")
+    mem_guard()
     for name in a.cases:
         run_case(name, a.out)
 

@@ -4,6 +4,6 @@ mkdir -p gpurun_out/golden
 export OMP_NUM_THREADS=$(nproc) OMP_PROC_BIND=close ORACLE_LEAN_TANGENTS=1
 make -s -C oracle
 for c in "$@"; do
-  ( /usr/bin/time -v python tools/fullsize_fixtures.py $c --out gpurun_out/golden ) > gpurun_out/golden/log_$c.txt 2>&1
+  python tools/fullsize_fixtures.py $c --out gpurun_out/golden > gpurun_out/golden/log_$c.txt 2>&1
   echo "rc $?" >> gpurun_out/golden/log_$c.txt
 done
