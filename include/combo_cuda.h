@@ -176,6 +176,25 @@ int combo_normals(combo_ctx* ctx, const uint8_t* img, const int64_t dims[3], con
                   const int64_t factors[3], const uint8_t* kind, int method, int centering,
                   int min_interface_voxels, double* normal3, uint8_t* flags, combo_normal_stats* stats,
                   int mem);
+/* Slab (plane-window) forms for the multi-GPU decomposition (no reference
+ * counterpart: the reference builds whole images, image.cpp:57-86):
+ * combo_generate_planes writes fine planes [plane0, plane0 + nplanes)
+ * (mod dims[0]) of the image combo_generate would produce for dims -- the
+ * same voxels bit for bit -- into out [nplanes][dims[1]][dims[2]]; `seed`
+ * is the full 64-bit generator seed of the seeded shapes 4, 10, 11, 12
+ * (their params[0] is ignored; combo_generate passes uint64(params[0])).
+ * combo_normals_slab computes the normals of boxel planes [bp0, bp0 + nbp)
+ * from an image window of planes [img0, img0 + img_planes) (mod dims[0])
+ * holding those boxels' fine planes plus one halo plane on each side (the
+ * Laplace stencil, normals.cpp:39-46); kind / normal3 / flags hold the nbp
+ * boxel planes. combo_coarsen needs no halo: pass the slab's fine planes. */
+int combo_generate_planes(combo_ctx* ctx, int shape, const int64_t dims[3], const double lengths[3],
+                          const double* params, int nparams, uint64_t seed, int64_t plane0, int64_t nplanes,
+                          uint8_t* out, int mem);
+int combo_normals_slab(combo_ctx* ctx, const uint8_t* img, int64_t img0, int64_t img_planes,
+                       const int64_t dims[3], const double lengths[3], const int64_t factors[3], int64_t bp0,
+                       int64_t nbp, const uint8_t* kind, int method, int centering, int min_interface_voxels,
+                       double* normal3, uint8_t* flags, combo_normal_stats* stats, int mem);
 
 /* ------------------------------------------------------- slab decomposition */
 /* Multi-GPU layout of SURVEY.md 8e (the reference is single-process OpenMP,
@@ -216,6 +235,16 @@ int combo_bind_materials(combo_ctx* ctx, const int64_t dims[3], const double len
                          const uint8_t* kind, const double* c_plus, const double* normal3,
                          const combo_law* matrix, const combo_law* inclusion, int combo,
                          const combo_laminate_opts* lam, int mem);
+/* the same from this process's slabs only (one rank per process: its n1/R
+ * boxel planes; emulated ranks: the whole grid), e.g. built per slab with
+ * combo_generate_planes / combo_coarsen / combo_normals_slab */
+int combo_bind_materials_slab(combo_ctx* ctx, const int64_t dims[3], const double lengths[3],
+                              const uint8_t* kind, const double* c_plus, const double* normal3,
+                              const combo_law* matrix, const combo_law* inclusion, int combo,
+                              const combo_laminate_opts* lam, int mem);
+/* number of bindings made on ctx so far (a CellMaterials handle records it
+ * and refuses to run once another binding replaced its materials) */
+int combo_bind_generation(const combo_ctx* ctx, int64_t* gen);
 int combo_composite_cells(const combo_ctx* ctx, int64_t* count);
 int combo_stress_floor(const combo_ctx* ctx, double* floor);
 /* warm starts (jump vectors) per composite id, 3 doubles each */

@@ -463,7 +463,9 @@ char* oracle_solve(void* h, const double* fbar9, const oracle_solver_cfg* c, dou
     js << "{\"success\":" << (rep.success ? "true" : "false") << ",\"error\":\"" << rep.error
        << "\",\"bisections\":" << rep.bisections << ",\"alpha\":" << fmt(rep.alpha)
        << ",\"seconds_total\":" << fmt(rep.seconds_total) << ",\"ls_total\":" << rep.ls_total
-       << ",\"steps\":[";
+       << ",\"ls_clock\":[";
+    for (std::size_t i = 0; i < rep.ls_clock.size(); ++i) js << (i ? "," : "") << fmt(rep.ls_clock[i]);
+    js << "],\"steps\":[";
     for (std::size_t s = 0; s < rep.steps.size(); ++s) {
       const auto& st = rep.steps[s];
       if (s) js << ",";

@@ -423,6 +423,7 @@ struct ConvergenceReport {
   double alpha = 0.0;
   double seconds_total = 0.0;
   std::int64_t ls_total = 0;  // Green-operator applications (LS iterations)
+  std::vector<double> ls_clock;  // seconds since solve() began, at the end of each LS iteration
 };
 struct SolveResult {
   Field9 f, p;

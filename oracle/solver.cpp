@@ -808,7 +808,7 @@ struct LsBudgetExhausted {};
 class CellSolver {
  public:
   CellSolver(CellMaterials& cm, const SolverConfig& cfg)
-      : cm_(cm), cfg_(cfg), grid_(cm.grid()), green_(cfg.green, cm.grid()),
+      : t0_(Clock::now()), cm_(cm), cfg_(cfg), grid_(cm.grid()), green_(cfg.green, cm.grid()),
         fft_(cm.grid().dims, 9), p_(cm.grid()), proj_(cm.grid()) {
     double lo, hi;
     cm_.spectrum_bounds(Mat3::identity(), lo, hi);
@@ -823,6 +823,7 @@ class CellSolver {
   double alpha() const { return alpha_; }
   DfmgState& dfmg_state() { return dfmg_state_; }
   std::int64_t ls_total = 0;
+  std::vector<double> ls_clock;  // end of every LS iteration (CPU-baseline timing)
   StepReport partial;  // the step cut short by the LS budget
 
  private:
@@ -830,6 +831,7 @@ class CellSolver {
     if (cfg_.max_ls_iterations > 0 && ls_total >= cfg_.max_ls_iterations) throw LsBudgetExhausted{};
     ++ls_total;
     green_.project(in, out, fft_);
+    ls_clock.push_back(seconds_since(t0_));
   }
   SweepStats eval_stress(const Field9& f) {
     if (cfg_.eval == kDfmg) return dfmg_stress(cm_, dfmg_state_, f, p_);
@@ -870,6 +872,7 @@ class CellSolver {
   bool run_newton(Field9& f, const Mat3& fbar, StepReport& rep);
   int cg_solve(Field9& x, const Field9& b, double tol_rel, bool& breakdown, StepReport& rep);
 
+  Clock::time_point t0_;
   CellMaterials& cm_;
   SolverConfig cfg_;
   SimGrid grid_;
@@ -1093,6 +1096,7 @@ SolveResult solve(CellMaterials& cm, const Mat3& fbar_target, const SolverConfig
   }
   report.alpha = solver.alpha();
   report.ls_total = solver.ls_total;
+  report.ls_clock = solver.ls_clock;
   report.seconds_total = seconds_since(tic);
   out.p = solver.stress();
   out.pbar = solver.pbar();

@@ -39,7 +39,15 @@ def error_type(e):
         if isinstance(e, cls):
             return name
     if isinstance(e, ComboError):
-        return e.type
+        # combo::Error subclasses by name, any other combo::Error ->
+        # SolverFailed; device / NCCL / allocation / API-misuse failures are
+        # not combo::Error in the reference -> InternalError
+        if e.type in ("ConfigInvalid", "BadShapeSpec", "NonDividingFactor", "LoadPathFailed",
+                      "InadmissibleMacroState"):
+            return e.type
+        if e.type in ("CudaError", "NcclError", "OutOfMemory", "BadArgument", "BadState"):
+            return "InternalError"
+        return "SolverFailed"
     if isinstance(e, RuntimeError) and str(e).startswith("SolverFailed"):
         return "SolverFailed"
     return "InternalError"

@@ -97,6 +97,13 @@ SIGNATURES = {
     "combo_laplace_weights": (C.c_int, [_VP, _VP, _I64, _D, _VP, C.c_int]),
     "combo_normals": (C.c_int, [_VP, _VP, _I64, _D, _I64, _VP, C.c_int, C.c_int, C.c_int, _VP, _VP,
                                 C.POINTER(NormalStats), C.c_int]),
+    "combo_generate_planes": (C.c_int, [_VP, C.c_int, _I64, _D, _D, C.c_int, C.c_uint64, C.c_int64, C.c_int64,
+                                        _VP, C.c_int]),
+    "combo_normals_slab": (C.c_int, [_VP, _VP, C.c_int64, C.c_int64, _I64, _D, _I64, C.c_int64, C.c_int64, _VP,
+                                     C.c_int, C.c_int, C.c_int, _VP, _VP, C.POINTER(NormalStats), C.c_int]),
+    "combo_bind_materials_slab": (C.c_int, [_VP, _I64, _D, _VP, _VP, _VP, C.POINTER(Law), C.POINTER(Law),
+                                            C.c_int, C.POINTER(LamOpts), C.c_int]),
+    "combo_bind_generation": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
     "combo_set_grid": (C.c_int, [_VP, _I64, _D]),
     "combo_nccl_unique_id": (C.c_int, [_VP]),
     "combo_ctx_set_virtual_ranks": (C.c_int, [_VP, C.c_int]),
@@ -307,17 +314,27 @@ class Context:
         return json.loads(self.L.combo_profile_json(self.h).decode())
 
     # ------------------------------------------------------------ images
-    def generate(self, shape, dims, lengths=(1.0, 1.0, 1.0), *params, out=None):
+    SHAPES = {"sphere": 0, "octahedron": 1, "fiber": 2, "cross_ply": 3, "fiber_pack": 4, "slab": 5,
+              "rsa_spheres": 10, "rsa_fibers_z": 11, "boolean_ellipsoids": 12}
+    SEEDED = ("fiber_pack", "rsa_spheres", "rsa_fibers_z", "boolean_ellipsoids")
+
+    def generate(self, shape, dims, lengths=(1.0, 1.0, 1.0), *params, out=None, seed=None, planes=None):
         """generate_* (image.cpp:57-227) and the seeded config generators;
-        `out` may be a CUDA uint8 tensor (device result)."""
-        ids = {"sphere": 0, "octahedron": 1, "fiber": 2, "cross_ply": 3, "fiber_pack": 4, "slab": 5, "rsa_spheres": 10, "rsa_fibers_z": 11,
-               "boolean_ellipsoids": 12}
+        `out` may be a CUDA uint8 tensor (device result). Seeded shapes take
+        their seed as params[0] (a Python int is exact to 64 bits) or
+        `seed`; planes = (plane0, nplanes) generates that window of fine
+        planes (mod dims[0]) only, bit-identical to the whole image's."""
+        dims = tuple(int(d) for d in dims)
+        plane0, nplanes = (0, dims[0]) if planes is None else (int(planes[0]), int(planes[1]))
+        if seed is None:
+            seed = int(params[0]) if shape in self.SEEDED and params else 0
         if out is None:
-            out = np.zeros(int(np.prod(dims)), dtype=np.uint8)
-        p = _f64(list(params) + [0.0] * (8 - len(params)))
-        self._check(self.L.combo_generate(self.h, ids[shape], _i64(dims), _f64(lengths), p, len(params),
-                                          _ptr(out), _mem(out)))
-        return out.reshape(tuple(dims))
+            out = np.zeros(nplanes * dims[1] * dims[2], dtype=np.uint8)
+        p = _f64([float(x) for x in params] + [0.0] * (8 - len(params)))
+        self._check(self.L.combo_generate_planes(self.h, self.SHAPES[shape], _i64(dims), _f64(lengths), p,
+                                                 len(params), C.c_uint64(int(seed) & (2**64 - 1)), plane0, nplanes,
+                                                 _ptr(out), _mem(out)))
+        return out.reshape((nplanes,) + dims[1:])
 
     def coarsen(self, img, factors, dims=None):
         """coarsen (combo_grid.cpp:28-71) -> kind, c_plus, count_plus (device
@@ -373,6 +390,40 @@ class Context:
                                          _ptr(kind), m, cen, int(min_interface_voxels), _ptr(n3), _ptr(flags),
                                          C.byref(st), _mem(img, kind)))
         return n3.reshape(nb, 3), flags, (st.composite, st.degenerate_fallbacks, st.too_few_fallbacks)
+
+    def compute_normals_slab(self, img, img0, dims, factors, bp0, nbp, kind, lengths=(1.0, 1.0, 1.0),
+                             method="second_moment", centering="weighted_centroid", min_interface_voxels=3):
+        """compute_normals for boxel planes [bp0, bp0 + nbp) from the image
+        window of fine planes starting at global plane img0 (mod dims[0])
+        that holds them plus one halo plane each side -> (nbp*b2*b3, 3),
+        flags, stats"""
+        dims = tuple(int(d) for d in dims)
+        nb = int(kind.numel() if _is_dev(kind) else np.asarray(kind).size)
+        img_planes = (int(img.numel()) if _is_dev(img) else int(np.asarray(img).size)) // (dims[1] * dims[2])
+        if _is_dev(img):
+            import torch
+
+            n3 = torch.empty(3 * nb, dtype=torch.float64, device=img.device)
+            flags = torch.empty(nb, dtype=torch.uint8, device=img.device)
+        else:
+            img = np.ascontiguousarray(img, dtype=np.uint8)
+            kind = np.ascontiguousarray(kind, dtype=np.uint8)
+            n3 = np.zeros(3 * nb)
+            flags = np.zeros(nb, np.uint8)
+        st = NormalStats()
+        m = {"barycenter": 0, "second_moment": 1}[method]
+        cen = {"weighted_centroid": 0, "boxel_center": 1}[centering]
+        self._check(self.L.combo_normals_slab(self.h, _ptr(img), int(img0), img_planes, _i64(dims), _f64(lengths),
+                                              _i64(factors), int(bp0), int(nbp), _ptr(kind), m, cen,
+                                              int(min_interface_voxels), _ptr(n3), _ptr(flags), C.byref(st),
+                                              _mem(img, kind)))
+        return n3.reshape(nb, 3), flags, (st.composite, st.degenerate_fallbacks, st.too_few_fallbacks)
+
+    @property
+    def bind_generation(self):
+        v = C.c_int64()
+        self._check(self.L.combo_bind_generation(self.h, C.byref(v)))
+        return int(v.value)
 
     # ------------------------------------------------ slab decomposition
     def set_virtual_ranks(self, nranks):
@@ -443,7 +494,11 @@ class CellMaterials:
     """CellMaterials (cell_material.hpp:19-74) bound on the device."""
 
     def __init__(self, ctx, dims, kind, c_plus, normal, matrix, inclusion, combo=True, opts=None,
-                 lengths=(1.0, 1.0, 1.0)):
+                 lengths=(1.0, 1.0, 1.0), local=False):
+        """kind / c_plus / normal describe the whole grid, or with local=True
+        this process's slabs only (combo_bind_materials_slab). The materials
+        live in the context: binding another CellMaterials on the same
+        context retires this one (its calls then raise BadState)."""
         self.ctx = ctx
         self.dims = tuple(int(d) for d in dims)
         self.lengths = tuple(float(x) for x in lengths)
@@ -453,39 +508,45 @@ class CellMaterials:
             c_plus = _f64(c_plus).ravel()
             normal = None if normal is None else _f64(normal).ravel()
         oc = (opts or LaminateOptions()).c()
-        ctx._check(ctx.L.combo_bind_materials(ctx.h, _i64(self.dims), _f64(self.lengths), _ptr(kind),
-                                              _ptr(c_plus), _ptr(normal), C.byref(matrix), C.byref(inclusion),
-                                              int(combo), C.byref(oc), _mem(kind, c_plus, normal)))
+        bind = ctx.L.combo_bind_materials_slab if local else ctx.L.combo_bind_materials
+        ctx._check(bind(ctx.h, _i64(self.dims), _f64(self.lengths), _ptr(kind), _ptr(c_plus), _ptr(normal),
+                        C.byref(matrix), C.byref(inclusion), int(combo), C.byref(oc), _mem(kind, c_plus, normal)))
+        self._gen = ctx.bind_generation
+
+    def _h(self):
+        if self.ctx.bind_generation != self._gen:
+            raise ComboError(-14, "CellMaterials: the context has been re-bound to other materials")
+        return self.ctx.h
 
     def reset_warm_starts(self):
         """CellMaterials::reset_warm_starts (cell_material.cpp:64-66)"""
-        self.ctx._check(self.ctx.L.combo_reset_warm_starts(self.ctx.h))
+        self.ctx._check(self.ctx.L.combo_reset_warm_starts(self._h()))
 
     @property
     def composites(self):
         v = C.c_int64()
-        self.ctx._check(self.ctx.L.combo_composite_cells(self.ctx.h, C.byref(v)))
+        self.ctx._check(self.ctx.L.combo_composite_cells(self._h(), C.byref(v)))
         return int(v.value)
 
     @property
     def stress_floor(self):
         v = C.c_double()
-        self.ctx._check(self.ctx.L.combo_stress_floor(self.ctx.h, C.byref(v)))
+        self.ctx._check(self.ctx.L.combo_stress_floor(self._h(), C.byref(v)))
         return float(v.value)
 
     def warm(self, value=None):
         buf = np.zeros(3 * self.composites)
         if value is None:
-            self.ctx._check(self.ctx.L.combo_get_warm_starts(self.ctx.h, _ptr(buf), MEM_HOST))
+            self.ctx._check(self.ctx.L.combo_get_warm_starts(self._h(), _ptr(buf), MEM_HOST))
             return buf.reshape(-1, 3)
         buf[:] = np.asarray(value, dtype=np.float64).ravel()
-        self.ctx._check(self.ctx.L.combo_set_warm_starts(self.ctx.h, _ptr(buf), MEM_HOST))
+        self.ctx._check(self.ctx.L.combo_set_warm_starts(self._h(), _ptr(buf), MEM_HOST))
 
     def stress_sweep(self, F):
         F = _f64(F).ravel()
         P = np.zeros_like(F)
         st = SweepStats()
-        self.ctx._check(self.ctx.L.combo_stress_sweep(self.ctx.h, _ptr(F), _ptr(P), C.byref(st), MEM_HOST))
+        self.ctx._check(self.ctx.L.combo_stress_sweep(self._h(), _ptr(F), _ptr(P), C.byref(st), MEM_HOST))
         return P, (st.inadmissible_cells, st.laminate_failures, st.back_projections, st.laminate_iter_max)
 
     def phase_averages(self, F):
@@ -495,7 +556,7 @@ class CellMaterials:
         mem = _mem(F)
         if mem == MEM_HOST:
             F = _f64(F).ravel()
-        self.ctx._check(self.ctx.L.combo_phase_averages(self.ctx.h, _ptr(F), C.byref(o), mem))
+        self.ctx._check(self.ctx.L.combo_phase_averages(self._h(), _ptr(F), C.byref(o), mem))
         m = lambda a: np.array(a[:]).reshape(3, 3)  # noqa: E731
         return dict(pbar=m(o.pbar), pbar_plus=m(o.pbar_plus), pbar_minus=m(o.pbar_minus), c_plus=o.c_plus,
                     has_plus=bool(o.has_plus), has_minus=bool(o.has_minus),
@@ -516,7 +577,7 @@ class CellMaterials:
             dev = F.device
             cell = torch.from_numpy(cell).to(dev)
             fp, fm, tr = (torch.from_numpy(a).to(dev) for a in (fp, fm, tr))
-        self.ctx._check(self.ctx.L.combo_recover_composites(self.ctx.h, _ptr(F), _ptr(cell), _ptr(fp), _ptr(fm),
+        self.ctx._check(self.ctx.L.combo_recover_composites(self._h(), _ptr(F), _ptr(cell), _ptr(fp), _ptr(fm),
                                                             _ptr(tr), mem))
         if mem != MEM_HOST:
             cell, fp, fm, tr = (a.cpu().numpy() for a in (cell, fp, fm, tr))
@@ -526,25 +587,33 @@ class CellMaterials:
 
     def tangent_matvec(self, F, x):
         y = np.zeros(9 * self.n)
-        self.ctx._check(self.ctx.L.combo_tangent_matvec(self.ctx.h, _ptr(_f64(F).ravel()), _ptr(_f64(x).ravel()),
+        self.ctx._check(self.ctx.L.combo_tangent_matvec(self._h(), _ptr(_f64(F).ravel()), _ptr(_f64(x).ravel()),
                                                         _ptr(y), MEM_HOST))
         return y
 
     def tangent45(self, F):
         t = np.zeros(45 * self.n)
-        self.ctx._check(self.ctx.L.combo_tangent45(self.ctx.h, _ptr(_f64(F).ravel()), _ptr(t), MEM_HOST))
+        self.ctx._check(self.ctx.L.combo_tangent45(self._h(), _ptr(_f64(F).ravel()), _ptr(t), MEM_HOST))
         return t
+
+    def tangent45_matvec(self, t45, x):
+        """tangent_matvec (cell_material.cpp:170-194) with caller-packed
+        tangents [cell][45] (pack45, cell_material.cpp:86-102)"""
+        y = np.zeros(9 * self.n)
+        self.ctx._check(self.ctx.L.combo_tangent45_matvec(self._h(), _ptr(_f64(t45).ravel()),
+                                                          _ptr(_f64(x).ravel()), _ptr(y), MEM_HOST))
+        return y
 
     def dfmg_stress(self, F):
         F = _f64(F).ravel()
         P = np.zeros_like(F)
         st = SweepStats()
-        self.ctx._check(self.ctx.L.combo_dfmg_stress(self.ctx.h, _ptr(F), _ptr(P), C.byref(st), MEM_HOST))
+        self.ctx._check(self.ctx.L.combo_dfmg_stress(self._h(), _ptr(F), _ptr(P), C.byref(st), MEM_HOST))
         return P, (st.inadmissible_cells, st.laminate_failures, st.back_projections, st.laminate_iter_max)
 
     def dfmg_tangent_matvec(self, F, x):
         y = np.zeros(9 * self.n)
-        self.ctx._check(self.ctx.L.combo_dfmg_tangent_matvec(self.ctx.h, _ptr(_f64(F).ravel()),
+        self.ctx._check(self.ctx.L.combo_dfmg_tangent_matvec(self._h(), _ptr(_f64(F).ravel()),
                                                              _ptr(_f64(x).ravel()), _ptr(y), MEM_HOST))
         return y
 
@@ -559,7 +628,7 @@ class CellMaterials:
         rep = C.c_void_p()
         cc = cfg.c()
         L = self.ctx.L
-        self.ctx._check(L.combo_solve(self.ctx.h, _f64(np.asarray(fbar).ravel()), C.byref(cc), _ptr(F), _ptr(P),
+        self.ctx._check(L.combo_solve(self._h(), _f64(np.asarray(fbar).ravel()), C.byref(cc), _ptr(F), _ptr(P),
                                       pbar, C.byref(rep), _mem(F, P)))
         report = json.loads(L.combo_report_json(rep).decode())
         L.combo_report_free(rep)

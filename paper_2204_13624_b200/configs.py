@@ -22,7 +22,7 @@ for the small parity cases; voxel-unit radii are scaled along.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -44,6 +44,7 @@ class Config:
     tol: float
     max_outer: int = 200
     voxel_params: tuple = field(default_factory=tuple)  # indices of params in voxel units
+    lengths: tuple = (1.0, 1.0, 1.0)
 
     @property
     def grid(self):
@@ -86,7 +87,59 @@ def scaled(cfg: Config, scale: int) -> Config:
     fine = tuple(max(f // scale, k) for f, k in zip(cfg.fine, cfg.factors))
     return Config(cfg.name + f"/{scale}", fine, cfg.factors, cfg.shape, tuple(p), cfg.matrix, cfg.inclusion,
                   cfg.fbar, cfg.load_steps, cfg.scheme, cfg.green, cfg.eval, cfg.tol, cfg.max_outer,
-                  cfg.voxel_params)
+                  cfg.voxel_params, cfg.lengths)
+
+
+# C5 weak-scaling ladder: P GPUs carry P x 512^3 boxels --
+# 512^3, 1024 x 512^2, 1024^2 x 512, 1024^3 (the 4096^3 -> 1024^3 scaling
+# config) -- with lengths proportional to the dims, so the voxel size, the
+# voxel-unit radii and the cubic boxels are those of the 1-GPU 512^3 case.
+LADDER = {1: (512, 512, 512), 2: (1024, 512, 512), 4: (1024, 1024, 512), 8: (1024, 1024, 1024)}
+
+
+def c5_ladder(P: int) -> Config:
+    if P not in LADDER:
+        raise ValueError(f"C5 ladder: no rung for {P} GPUs (1, 2, 4, 8)")
+    g = LADDER[P]
+    base = CONFIGS["C5"]
+    fine = tuple(4 * n for n in g)
+    lengths = tuple(n / 512.0 for n in g)
+    name = "C5" if P == 1 else f"C5x{P}"
+    return replace(base, name=name, fine=fine, lengths=lengths)
+
+
+def build_slab_grid(ctx, cfg: Config, nranks: int = 1, rank: int = 0):
+    """Device preprocessing of rank `rank`'s slab of boxel planes: the fine
+    planes of the slab plus one halo plane each side are generated
+    (combo_generate_planes), coarsened and given normals
+    (combo_normals_slab); nothing outside the window is built. Returns
+    (kind, c_plus, normals, normal stats) of the slab as CUDA tensors."""
+    import torch
+
+    f1, f2, f3 = cfg.fine
+    a1 = cfg.factors[0]
+    b1 = f1 // a1
+    if b1 % nranks:
+        raise ValueError("slab decomposition: the rank count must divide the boxel planes")
+    nbp = b1 // nranks
+    bp0 = rank * nbp
+    plane = f2 * f3
+    if nranks == 1:
+        img = torch.empty(f1 * plane, dtype=torch.uint8, device="cuda")
+        ctx.generate(cfg.shape, cfg.fine, cfg.lengths, *cfg.params, out=img)
+        kind, cp, cnt = ctx.coarsen(img, cfg.factors, dims=cfg.fine)
+        nrm, flags, st = ctx.compute_normals(img, cfg.factors, kind, lengths=cfg.lengths, dims=cfg.fine)
+    else:
+        f0, nf = bp0 * a1, nbp * a1
+        img = torch.empty((nf + 2) * plane, dtype=torch.uint8, device="cuda")
+        ctx.generate(cfg.shape, cfg.fine, cfg.lengths, *cfg.params, out=img, planes=(f0 - 1, nf + 2))
+        kind, cp, cnt = ctx.coarsen(img[plane:(nf + 1) * plane], cfg.factors, dims=(nf, f2, f3))
+        nrm, flags, st = ctx.compute_normals_slab(img, f0 - 1, cfg.fine, cfg.factors, bp0, nbp, kind,
+                                                  lengths=cfg.lengths)
+    ctx.synchronize()
+    del img, cnt, flags
+    torch.cuda.empty_cache()
+    return kind, cp, nrm, st
 
 
 def build_grid(ctx, cfg: Config):

@@ -124,6 +124,7 @@ struct FftPlan {
     s.n3c = n3c;
     s.n3p = n3p;
     s.blocked = R > 1 ? 1 : 0;
+    s.swap = swap ? 1 : 0;
     s.ni = ni;
     s.nj = nj;
     s.i0 = i0;
@@ -198,6 +199,7 @@ struct combo_ctx {
 
   // materials (combo_bind_materials)
   bool bound = false;
+  int64_t bind_gen = 0;  // bumped by every binding (stale CellMaterials handles)
   combo_law law_m{}, law_i{};
   combo_laminate_opts lam{};
   double stress_floor = 1e-300;
@@ -265,7 +267,8 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths);
 int ew_grid(int64_t n);
 void ensure_scratch(combo_ctx* c);
 void reduce_partials(combo_ctx* c, int64_t nblocks, int nred, int slot);
-void fetch_results(combo_ctx* c);  // dres + stats -> hres (sync)
+// dres (+ laminate stats, combined over NCCL ranks when with_stats) -> hres (sync)
+void fetch_results(combo_ctx* c, bool with_stats = true);
 combo_dev::LawP law_params(const combo_law& L, double* dev_a9);
 void ensure_partials(combo_ctx* c, int64_t count);
 // dfmg.cu

@@ -242,7 +242,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->spec.alloc(size_t(9 * p->ni * d[1] * p->n3p));
   if (R > 1) {
     p->specB.alloc(size_t(9 * p->ni * d[1] * p->n3p));
-    p->swap = false;
   }
   c->plan = std::move(p);
 }
@@ -261,9 +260,9 @@ void reduce_partials(combo_ctx* c, int64_t nblocks, int nred, int slot) {
   COMBO_CK(cudaGetLastError());
 }
 
-void fetch_results(combo_ctx* c) {
+void fetch_results(combo_ctx* c, bool with_stats) {
   const Stats* st = c->dstats.p;
-  if (c->nccl && c->R > 1) {
+  if (with_stats && c->nccl && c->R > 1) {
     // laminate statistics of all ranks: sums and the maximum iteration count
     c->gstats.alloc(1);
     nccl_allreduce_u64(c, reinterpret_cast<const unsigned long long*>(c->dstats.p),
@@ -908,7 +907,7 @@ class Solver {
   // pin_mean on F (field.cpp:28-38): materialize pending shift, sum, new shift
   void pin_mean(const double* target) {
     materialize_sum(0);
-    fetch_results(c_);
+    fetch_results(c_, false);
     for (int q = 0; q < 9; ++q) shF_.v[q] = target[q] - c_->hres[q] / double(Ng_);
   }
   void copy_all(int dst, int src) {
@@ -1048,7 +1047,7 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
             c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; }, cons, 20);
       }
     }
-    fetch_results(c_);
+    fetch_results(c_, false);
     const double pap = c_->hres[20];
     if (!(pap > 0.0)) {
       breakdown = true;
@@ -1067,7 +1066,7 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
       COMBO_CK(cudaGetLastError());
     }
     group_reduce(c_, nbc, 1, 21);
-    fetch_results(c_);
+    fetch_results(c_, false);
     ++it;
     step_prev = step;
     const double rr_new = c_->hres[21];
@@ -1104,7 +1103,7 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
       project_group(
           c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
           [&](size_t k) { return ConsResid{P(r_, k), rk_[k].N}; }, 9);
-      fetch_results(c_);
+      fetch_results(c_, false);
       ss = c_->hres[9];
     } else {
       rep.sweep = combo_sweep_stats{0, 0, 0, 0};
@@ -1152,7 +1151,7 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
         COMBO_CK(cudaGetLastError());
       }
       group_reduce(c_, nbc, 9, 30);
-      fetch_results(c_);
+      fetch_results(c_, false);
       for (int q = 0; q < 9; ++q) sh_t.v[q] = fbar[q] - c_->hres[30 + q] / double(Ng_);
       reset_stats(c_);
       eval_sweep(Fo_, sh_t, 0.0, rb_, true, 0);
@@ -1168,7 +1167,7 @@ bool Solver::run_newton(const double* fbar, combo_host::StepRec& rep) {
         project_group(
             c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
             [&](size_t k) { return ConsResid{P(bn_, k), rk_[k].N}; }, 9);
-        fetch_results(c_);
+        fetch_results(c_, false);
         const double ss_t = c_->hres[9];
         std::memcpy(pbar_, pb, sizeof pb);  // residual_from_stress sets pbar_ (:95)
         const double rtrial = std::sqrt(ss_t / double(Ng_)) / std::max(norm9(pb), stress_floor_);
@@ -1573,14 +1572,15 @@ int combo_slab_row(const int64_t dims[3], int nranks, int rank, int side, int64_
   v.n3c = dims[2] / 2 + 1;
   v.n3p = (v.n3c + 7) / 8 * 8;
   v.blocked = nranks > 1;
+  v.swap = 1;  // the default layout (COMBO_SWAP=1)
   v.ni = dims[0] / nranks;
   v.nj = dims[1] / nranks;
   v.i0 = rank * v.ni;
   v.j0 = rank * v.nj;
   v.blk = 9 * v.ni * v.nj * v.n3p;
   v.cs = nranks > 1 ? v.ni * v.nj * v.n3p : v.n1 * v.n2 * v.n3p;
-  v.si = v.n2 * v.n3p;
-  v.sj = v.n3p;
+  v.si = v.n3p;  // j-major rows (COMBO_SWAP=1)
+  v.sj = v.n1 * v.n3p;
   *off = c * v.cs + (side == 0 ? v.rowA(i, j) : v.rowB(i, j));
   return COMBO_OK;
 }
@@ -1667,20 +1667,45 @@ static void bind_slab(combo_ctx* c, const int64_t dims[3], const double lengths[
 
 extern "C" {
 
-// the arrays describe the whole grid; every rank binds its slab of planes
-int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengths[3], const uint8_t* kind,
-                         const double* c_plus, const double* normal3, const combo_law* matrix,
-                         const combo_law* inclusion, int combo, const combo_laminate_opts* lam, int mem) {
+namespace {
+// local: the arrays hold this process's slabs only (its ranks' planes, in
+// rank order) instead of the whole grid
+int bind_members(combo_ctx* c, const int64_t dims[3], const double lengths[3], const uint8_t* kind,
+                 const double* c_plus, const double* normal3, const combo_law* matrix, const combo_law* inclusion,
+                 int combo, const combo_laminate_opts* lam, int mem, bool local) {
   return guarded(c, [&] {
     if (!kind || !c_plus || !matrix || !inclusion) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
     for (combo_ctx* m : members(c)) {
       m->R = c->R;
       set_grid(m, dims, lengths);
-      const int64_t off = int64_t(m->q) * m->N;
+      const int64_t off = int64_t(local ? m->q - c->q : m->q) * m->N;
       bind_slab(m, dims, lengths, kind + off, c_plus + off, normal3 ? normal3 + 3 * off : nullptr, matrix, inclusion,
                 combo, lam, mem);
     }
+    ++c->bind_gen;
   });
+}
+}  // namespace
+
+// the arrays describe the whole grid; every rank binds its slab of planes
+int combo_bind_materials(combo_ctx* c, const int64_t dims[3], const double lengths[3], const uint8_t* kind,
+                         const double* c_plus, const double* normal3, const combo_law* matrix,
+                         const combo_law* inclusion, int combo, const combo_laminate_opts* lam, int mem) {
+  return bind_members(c, dims, lengths, kind, c_plus, normal3, matrix, inclusion, combo, lam, mem, false);
+}
+
+// the arrays hold this process's slabs (one rank per process: its own
+// n1/R planes), e.g. from combo_generate_planes / combo_normals_slab
+int combo_bind_materials_slab(combo_ctx* c, const int64_t dims[3], const double lengths[3], const uint8_t* kind,
+                              const double* c_plus, const double* normal3, const combo_law* matrix,
+                              const combo_law* inclusion, int combo, const combo_laminate_opts* lam, int mem) {
+  return bind_members(c, dims, lengths, kind, c_plus, normal3, matrix, inclusion, combo, lam, mem, true);
+}
+
+int combo_bind_generation(const combo_ctx* c, int64_t* gen) {
+  if (!c || !gen) return COMBO_ERR_BAD_ARGUMENT;
+  *gen = c->bind_gen;
+  return COMBO_OK;
 }
 
 int combo_composite_cells(const combo_ctx* c, int64_t* count) {

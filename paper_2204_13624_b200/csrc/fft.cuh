@@ -284,17 +284,20 @@ struct SpecView {
   int64_t si, sj;                // single-slab row strides
   int64_t ni, nj, i0, j0, blk;   // slab / pencil extents and offsets
   int blocked;
+  int swap;  // blocked: rows j-major inside each block (x lines contiguous), else i-major
   // slab side: local plane il, global k2 j
   __host__ __device__ __forceinline__ int64_t rowA(int64_t il, int64_t j) const {
     if (!blocked) return il * si + j * sj;
     const int s = int(j) / int(nj);
-    return s * blk + (il * nj + (j - int64_t(s) * nj)) * n3p;
+    const int64_t jl = j - int64_t(s) * nj;
+    return s * blk + (swap ? jl * ni + il : il * nj + jl) * n3p;
   }
   // pencil side: global plane i, local k2 jl
   __host__ __device__ __forceinline__ int64_t rowB(int64_t i, int64_t jl) const {
     if (!blocked) return i * si + jl * sj;
     const int r = int(i) / int(ni);
-    return r * blk + ((i - int64_t(r) * ni) * nj + jl) * n3p;
+    const int64_t il = i - int64_t(r) * ni;
+    return r * blk + (swap ? jl * ni + il : il * nj + jl) * n3p;
   }
   // row of component c on local z-line `line` = il n2 + j
   __host__ __device__ __forceinline__ int64_t zrow(int64_t c, int64_t line) const {

@@ -30,11 +30,20 @@ __device__ __forceinline__ int64_t wrapi(int64_t a, int64_t n) {
   return a < 0 ? a + n : a;
 }
 
+// A window of fine planes [i0, i0 + planes) (mod n1) of the n1 x n2 x n3
+// image: at() takes global (wrapped) plane indices. The whole image is the
+// window i0 = 0; a slab rank's window adds one halo plane on each side
+// (the Laplace stencil of the second-moment normals, normals.cpp:39-46).
 struct ImgView {
   const uint8_t* p;
   int64_t n1, n2, n3;
   double h1, h2, h3;
-  __device__ __forceinline__ uint8_t at(int64_t i, int64_t j, int64_t k) const { return p[(i * n2 + j) * n3 + k]; }
+  int64_t i0 = 0;
+  __device__ __forceinline__ uint8_t at(int64_t i, int64_t j, int64_t k) const {
+    int64_t li = i - i0;
+    if (li < 0) li += n1;
+    return p[(li * n2 + j) * n3 + k];
+  }
 };
 
 __global__ void k_coarsen(ImgView im, int64_t f1, int64_t f2, int64_t f3, int64_t b1, int64_t b2, int64_t b3,
@@ -155,6 +164,7 @@ __device__ void smallest_eigvec(const double* m, double* out) {
 struct NormalArgs {
   ImgView im;
   int64_t f1, f2, f3, b1, b2, b3;
+  int64_t bp0, nbp;  // boxel planes [bp0, bp0 + nbp) of the grid (kind / outputs: local)
   double bl0, bl1, bl2;  // boxel lengths
   double r1, r2, r3;
   int method, centering, min_support;
@@ -162,12 +172,12 @@ struct NormalArgs {
 
 __global__ void k_normals(NormalArgs A, const uint8_t* kind, double* normal3, uint8_t* flags,
                           unsigned long long* stats) {
-  const int64_t nb = A.b1 * A.b2 * A.b3;
+  const int64_t nb = A.nbp * A.b2 * A.b3;
   const ImgView& im = A.im;
   for (int64_t ib = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; ib < nb; ib += int64_t(gridDim.x) * blockDim.x) {
     if (kind[ib] != 2) continue;
     atomicAdd(stats, 1ull);
-    const int64_t bk = ib % A.b3, bj = (ib / A.b3) % A.b2, bi = ib / (A.b2 * A.b3);
+    const int64_t bk = ib % A.b3, bj = (ib / A.b3) % A.b2, bi = A.bp0 + ib / (A.b2 * A.b3);
     // barycenter normal (normals.cpp:87-137)
     double sp[3] = {0, 0, 0}, smn[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     int64_t np = 0, nm = 0;
@@ -293,6 +303,7 @@ struct GenArgs {
   double L[3], h[3];
   int shape;
   double p[8];
+  int64_t plane0 = 0, nplanes = 0;  // output window: global planes [plane0, plane0 + nplanes) mod n1
 };
 
 // image.cpp:88-227 predicates (same arithmetic, --fmad=false)
@@ -343,9 +354,9 @@ __device__ bool predicate(const GenArgs& g, double x, double y, double z) {
 }
 
 __global__ void k_generate(GenArgs g, uint8_t* out) {
-  const int64_t n = g.n1 * g.n2 * g.n3;
+  const int64_t n = g.nplanes * g.n2 * g.n3;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t k = v % g.n3, j = (v / g.n3) % g.n2, i = v / (g.n2 * g.n3);
+    const int64_t k = v % g.n3, j = (v / g.n3) % g.n2, i = wrapi(g.plane0 + v / (g.n2 * g.n3), g.n1);
     const double x = (double(i) + 0.5) * g.h[0];
     const double y = (double(j) + 0.5) * g.h[1];
     const double z = (double(k) + 0.5) * g.h[2];
@@ -357,9 +368,9 @@ __global__ void k_generate(GenArgs g, uint8_t* out) {
 // list (centre, unit axis; generated on the host from the seed)
 __global__ void k_generate_pack(GenArgs g, const double* __restrict__ fib, int count, double hl, double radius,
                                 uint8_t* out) {
-  const int64_t n = g.n1 * g.n2 * g.n3;
+  const int64_t n = g.nplanes * g.n2 * g.n3;
   for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t k = v % g.n3, j = (v / g.n3) % g.n2, i = v / (g.n2 * g.n3);
+    const int64_t k = v % g.n3, j = (v / g.n3) % g.n2, i = wrapi(g.plane0 + v / (g.n2 * g.n3), g.n1);
     const double x[3] = {(double(i) + 0.5) * g.h[0], (double(j) + 0.5) * g.h[1], (double(k) + 0.5) * g.h[2]};
     uint8_t in = 0;
     for (int f = 0; f < count && !in; ++f) {
@@ -388,8 +399,11 @@ struct Obj {
   int type;       // 0 sphere, 1 z-cylinder, 2 ellipsoid
 };
 
+// objects -> voxels of the plane window [plane0, plane0 + nplanes) (mod n1)
+// of the image; one block per object, plane by plane (planes outside the
+// window cost one test)
 __global__ void k_raster(const Obj* objs, int64_t nobj, int64_t n1, int64_t n2, int64_t n3, double L0, double L1,
-                         double L2, double h0, double h1, double h2, uint8_t* out) {
+                         double L2, double h0, double h1, double h2, int64_t plane0, int64_t nplanes, uint8_t* out) {
   for (int64_t o = blockIdx.x; o < nobj; o += gridDim.x) {
     const Obj ob = objs[o];
     const int64_t i0 = int64_t(floor((ob.c[0] - ob.r) / h0)) - 1, i1 = int64_t(floor((ob.c[0] + ob.r) / h0)) + 1;
@@ -400,25 +414,33 @@ __global__ void k_raster(const Obj* objs, int64_t nobj, int64_t n1, int64_t n2, 
       k1 = n3 - 1;
     }
     const int64_t ni = min(i1 - i0 + 1, n1), nj = min(j1 - j0 + 1, n2), nk = min(k1 - k0 + 1, n3);
-    const int64_t tot = ni * nj * nk;
-    for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
-      const int64_t kk = t % nk, jj = (t / nk) % nj, ii = t / (nj * nk);
-      const int64_t i = wrapi(i0 + ii, n1), j = wrapi(j0 + jj, n2), k = wrapi(k0 + kk, n3);
-      const double x = (double(i) + 0.5) * h0, y = (double(j) + 0.5) * h1, z = (double(k) + 0.5) * h2;
-      const double dx = wrapd(x - ob.c[0], L0), dy = wrapd(y - ob.c[1], L1), dz = wrapd(z - ob.c[2], L2);
-      bool in;
-      if (ob.type == 0) {
-        in = dx * dx + dy * dy + dz * dz < ob.a[0] * ob.a[0];
-      } else if (ob.type == 1) {
-        in = dx * dx + dy * dy < ob.a[0] * ob.a[0];
-      } else {
-        const double b0 = ob.R[0] * dx + ob.R[3] * dy + ob.R[6] * dz;
-        const double b1 = ob.R[1] * dx + ob.R[4] * dy + ob.R[7] * dz;
-        const double b2 = ob.R[2] * dx + ob.R[5] * dy + ob.R[8] * dz;
-        const double q = (b0 / ob.a[0]) * (b0 / ob.a[0]) + (b1 / ob.a[1]) * (b1 / ob.a[1]) + (b2 / ob.a[2]) * (b2 / ob.a[2]);
-        in = q < 1.0;
+    const int64_t tot = nj * nk;
+    for (int64_t ii = 0; ii < ni; ++ii) {
+      const int64_t i = wrapi(i0 + ii, n1);
+      const int64_t li = wrapi(i - plane0, n1);
+      if (li >= nplanes) continue;
+      const double x = (double(i) + 0.5) * h0;
+      const double dx = wrapd(x - ob.c[0], L0);
+      for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
+        const int64_t kk = t % nk, jj = t / nk;
+        const int64_t j = wrapi(j0 + jj, n2), k = wrapi(k0 + kk, n3);
+        const double y = (double(j) + 0.5) * h1, z = (double(k) + 0.5) * h2;
+        const double dy = wrapd(y - ob.c[1], L1), dz = wrapd(z - ob.c[2], L2);
+        bool in;
+        if (ob.type == 0) {
+          in = dx * dx + dy * dy + dz * dz < ob.a[0] * ob.a[0];
+        } else if (ob.type == 1) {
+          in = dx * dx + dy * dy < ob.a[0] * ob.a[0];
+        } else {
+          const double b0 = ob.R[0] * dx + ob.R[3] * dy + ob.R[6] * dz;
+          const double b1 = ob.R[1] * dx + ob.R[4] * dy + ob.R[7] * dz;
+          const double b2 = ob.R[2] * dx + ob.R[5] * dy + ob.R[8] * dz;
+          const double q =
+              (b0 / ob.a[0]) * (b0 / ob.a[0]) + (b1 / ob.a[1]) * (b1 / ob.a[1]) + (b2 / ob.a[2]) * (b2 / ob.a[2]);
+          in = q < 1.0;
+        }
+        if (in) out[(li * n2 + j) * n3 + k] = 1;
       }
-      if (in) out[(i * n2 + j) * n3 + k] = 1;
     }
   }
 }
@@ -584,8 +606,13 @@ int grid_for(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n +
 
 extern "C" {
 
-int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double lengths[3], const double* params,
-                   int nparams, uint8_t* out, int mem) {
+// fine-image planes [plane0, plane0 + nplanes) (mod dims[0]) of the image
+// generate_* / the seeded config generators would produce for the whole
+// dims grid (same voxels bit for bit); seed: the generator seed of the
+// seeded shapes (4, 10, 11, 12), which ignore params[0]
+int combo_generate_planes(combo_ctx* c, int shape, const int64_t dims[3], const double lengths[3],
+                          const double* params, int nparams, uint64_t seed, int64_t plane0, int64_t nplanes,
+                          uint8_t* out, int mem) {
   return guarded(c, [&] {
     GenArgs g{};
     g.n1 = dims[0];
@@ -597,9 +624,12 @@ int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double 
       g.L[a] = lengths[a];
       g.h[a] = lengths[a] / double(dims[a]);
     }
+    if (nplanes < 1 || nplanes > dims[0]) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "generate: bad plane window");
+    g.plane0 = ((plane0 % dims[0]) + dims[0]) % dims[0];
+    g.nplanes = nplanes;
     g.shape = shape;
     for (int i = 0; i < nparams && i < 8; ++i) g.p[i] = params[i];
-    const int64_t n = g.n1 * g.n2 * g.n3;
+    const int64_t n = nplanes * g.n2 * g.n3;
     DBuf<uint8_t> tmp;
     uint8_t* d = dev_or_stage(c, out, size_t(n), mem, tmp, false);
     if (shape == 0 || shape == 1 || shape == 2 || shape == 3 || shape == 5) {
@@ -615,12 +645,12 @@ int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double 
       k_generate<<<grid_for(n), 256, 0, c->stream>>>(g, d);
       ++c->launches;
     } else if (shape == 4) {
-      // p = seed, count, radius, length, orientation_spread
+      // p = (seed), count, radius, length, orientation_spread
       const int count = int(g.p[1]);
       const double radius = g.p[2], length = g.p[3], spread = g.p[4];
       if (count < 0) throw ComboError(COMBO_ERR_BAD_SHAPE, "fiber_pack: count must be >= 0");
       if (radius < 0.0 || length < 0.0) throw ComboError(COMBO_ERR_BAD_SHAPE, "fiber_pack: radius/length");
-      Sm64 rng{uint64_t(g.p[0])};
+      Sm64 rng{seed};
       std::vector<double> fib(size_t(6) * size_t(std::max(count, 1)));
       for (int f = 0; f < count; ++f) {
         double* c = fib.data() + 6 * f;
@@ -641,10 +671,27 @@ int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double 
       COMBO_CK(cudaGetLastError());
       COMBO_CK(cudaStreamSynchronize(c->stream));
     } else if (shape >= 10 && shape <= 12) {
+      std::vector<Obj> all;
+      if (shape == 10) all = rsa(g, seed, g.p[1], g.p[2], g.p[3], false);
+      if (shape == 11) all = rsa(g, seed, g.p[1], g.p[1], g.p[2], true);
+      if (shape == 12) all = boolean_ellipsoids(g, seed, g.p[1], g.p[2], g.p[3]);
+      // objects whose plane range (k_raster's, widened by one plane for the
+      // host rounding) meets the window
       std::vector<Obj> objs;
-      if (shape == 10) objs = rsa(g, uint64_t(g.p[0]), g.p[1], g.p[2], g.p[3], false);
-      if (shape == 11) objs = rsa(g, uint64_t(g.p[0]), g.p[1], g.p[1], g.p[2], true);
-      if (shape == 12) objs = boolean_ellipsoids(g, uint64_t(g.p[0]), g.p[1], g.p[2], g.p[3]);
+      if (nplanes == g.n1) {
+        objs.swap(all);
+      } else {
+        for (const Obj& o : all) {
+          const int64_t a = int64_t(std::floor((o.c[0] - o.r) / g.h[0])) - 2;
+          const int64_t b = int64_t(std::floor((o.c[0] + o.r) / g.h[0])) + 2;
+          bool hit = b - a + 1 >= g.n1;
+          for (int64_t i = a; i <= b && !hit; ++i) {
+            const int64_t li = (((i - g.plane0) % g.n1) + g.n1) % g.n1;
+            hit = li < nplanes;
+          }
+          if (hit) objs.push_back(o);
+        }
+      }
       COMBO_CK(cudaMemsetAsync(d, 0, size_t(n), c->stream));
       DBuf<Obj> dobj;
       dobj.alloc(objs.size());
@@ -652,7 +699,8 @@ int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double 
       const int64_t blocks = std::min<int64_t>(int64_t(objs.size()), 148 * 64);
       if (blocks > 0) {
         k_raster<<<unsigned(blocks), 256, 0, c->stream>>>(dobj.p, int64_t(objs.size()), g.n1, g.n2, g.n3, g.L[0],
-                                                          g.L[1], g.L[2], g.h[0], g.h[1], g.h[2], d);
+                                                          g.L[1], g.L[2], g.h[0], g.h[1], g.h[2], g.plane0,
+                                                          g.nplanes, d);
         ++c->launches;
       }
       COMBO_CK(cudaStreamSynchronize(c->stream));
@@ -663,6 +711,13 @@ int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double 
     copy_back(c, out, d, size_t(n), mem);
     COMBO_CK(cudaStreamSynchronize(c->stream));
   });
+}
+
+// the whole image; seeded shapes take the seed from params[0]
+int combo_generate(combo_ctx* c, int shape, const int64_t dims[3], const double lengths[3], const double* params,
+                   int nparams, uint8_t* out, int mem) {
+  const uint64_t seed = (nparams > 0 && params && params[0] >= 0.0) ? uint64_t(params[0]) : 0;
+  return combo_generate_planes(c, shape, dims, lengths, params, nparams, seed, 0, dims ? dims[0] : 1, out, mem);
 }
 
 int combo_coarsen(combo_ctx* c, const uint8_t* img, const int64_t dims[3], const int64_t factors[3], uint8_t* kind,
@@ -711,9 +766,15 @@ int combo_laplace_weights(combo_ctx* c, const uint8_t* img, const int64_t dims[3
   });
 }
 
-int combo_normals(combo_ctx* c, const uint8_t* img, const int64_t dims[3], const double lengths[3],
-                  const int64_t factors[3], const uint8_t* kind, int method, int centering, int min_support,
-                  double* normal3, uint8_t* flags, combo_normal_stats* stats, int mem) {
+// compute_normals (normals.cpp:211-256) for boxel planes [bp0, bp0 + nbp) of
+// the grid of a dims image, from an image window of planes [img0, img0 +
+// img_planes) (mod dims[0]) that covers the boxels' fine planes plus one
+// halo plane on each side for the second-moment method (the whole image
+// qualifies). kind / normal3 / flags: the nbp boxel planes.
+int combo_normals_slab(combo_ctx* c, const uint8_t* img, int64_t img0, int64_t img_planes, const int64_t dims[3],
+                       const double lengths[3], const int64_t factors[3], int64_t bp0, int64_t nbp,
+                       const uint8_t* kind, int method, int centering, int min_support, double* normal3,
+                       uint8_t* flags, combo_normal_stats* stats, int mem) {
   return guarded(c, [&] {
     int64_t b[3];
     for (int a = 0; a < 3; ++a) {
@@ -721,7 +782,19 @@ int combo_normals(combo_ctx* c, const uint8_t* img, const int64_t dims[3], const
         throw ComboError(COMBO_ERR_NON_DIVIDING_FACTOR, "normals: factor does not divide image dims");
       b[a] = dims[a] / factors[a];
     }
-    const int64_t n = dims[0] * dims[1] * dims[2], nb = b[0] * b[1] * b[2];
+    if (nbp < 1 || bp0 < 0 || bp0 + nbp > b[0] || img_planes < 1 || img_planes > dims[0])
+      throw ComboError(COMBO_ERR_BAD_ARGUMENT, "normals: bad plane window");
+    const int64_t w0 = ((img0 % dims[0]) + dims[0]) % dims[0];
+    if (img_planes < dims[0]) {
+      // fine planes the kernel reads: the boxels' own, +-1 for the stencil
+      const int64_t need0 = bp0 * factors[0] - (method == 1 ? 1 : 0);
+      const int64_t need1 = (bp0 + nbp) * factors[0] + (method == 1 ? 1 : 0);
+      for (int64_t i = need0; i < need1; ++i) {
+        const int64_t li = (((i - w0) % dims[0]) + dims[0]) % dims[0];
+        if (li >= img_planes) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "normals: image window misses a needed plane");
+      }
+    }
+    const int64_t n = img_planes * dims[1] * dims[2], nb = nbp * b[1] * b[2];
     DBuf<uint8_t> ti, tk, tf;
     DBuf<double> tn;
     const uint8_t* di = dev_or_stage(c, const_cast<uint8_t*>(img), size_t(n), mem, ti, true);
@@ -735,13 +808,15 @@ int combo_normals(combo_ctx* c, const uint8_t* img, const int64_t dims[3], const
     COMBO_CK(cudaMemsetAsync(ds.p, 0, 24, c->stream));
     NormalArgs A{};
     const double h1 = lengths[0] / double(dims[0]), h2 = lengths[1] / double(dims[1]), h3 = lengths[2] / double(dims[2]);
-    A.im = ImgView{di, dims[0], dims[1], dims[2], h1, h2, h3};
+    A.im = ImgView{di, dims[0], dims[1], dims[2], h1, h2, h3, w0};
     A.f1 = factors[0];
     A.f2 = factors[1];
     A.f3 = factors[2];
     A.b1 = b[0];
     A.b2 = b[1];
     A.b3 = b[2];
+    A.bp0 = bp0;
+    A.nbp = nbp;
     A.bl0 = lengths[0] / double(b[0]);
     A.bl1 = lengths[1] / double(b[1]);
     A.bl2 = lengths[2] / double(b[2]);
@@ -765,6 +840,17 @@ int combo_normals(combo_ctx* c, const uint8_t* img, const int64_t dims[3], const
       stats->too_few_fallbacks = int64_t(hs[2]);
     }
   });
+}
+
+int combo_normals(combo_ctx* c, const uint8_t* img, const int64_t dims[3], const double lengths[3],
+                  const int64_t factors[3], const uint8_t* kind, int method, int centering, int min_support,
+                  double* normal3, uint8_t* flags, combo_normal_stats* stats, int mem) {
+  if (!dims || !factors || factors[0] < 1 || dims[0] % factors[0] != 0) {
+    if (c) c->err = "normals: factor does not divide image dims";
+    return COMBO_ERR_NON_DIVIDING_FACTOR;
+  }
+  return combo_normals_slab(c, img, 0, dims[0], dims, lengths, factors, 0, dims[0] / factors[0], kind, method,
+                            centering, min_support, normal3, flags, stats, mem);
 }
 
 int combo_laminate_solve(combo_ctx* c, const double fbox[9], const combo_law* plus, const combo_law* minus,

@@ -131,6 +131,10 @@ class RunConfig:
             c.conv = _get(n, "conv", "direct")
             if c.conv not in ("direct", "fft"):
                 raise ConfigInvalid(f"config: unknown conv \"{c.conv}\"")
+            if c.conv == "fft":
+                # normals.cpp:54-84 (FFT Laplace weights) is not on the device
+                # path; refuse it rather than silently using the direct stencil
+                raise ConfigInvalid("config: normals.conv \"fft\" is not supported (use \"direct\")")
         if "materials" in j:
             _reject_unknown(j["materials"], {"matrix", "inclusion"}, "materials")
             c.materials = copy.deepcopy(j["materials"])
@@ -308,7 +312,7 @@ def stage_generate(ctx, cfg):
     elif shape == "cross_ply":
         params = (float(g["radius"]), float(g["pitch"]), float(int(g["layers"])))
     elif shape == "fiber_pack":
-        params = (float(int(cfg.seed)), float(int(g["count"])), float(g["radius"]), float(g["length"]),
+        params = (int(cfg.seed), float(int(g["count"])), float(g["radius"]), float(g["length"]),
                   float(g["orientation_spread"]))
     else:
         raise ConfigInvalid(f"generate: shape \"{shape}\" is not generated on the device path")
@@ -501,7 +505,7 @@ def stage_bench(ctx, cfg, suite="sphere-smoke"):
         rows = [ref_row(img, "ref 100^3 (no combo)"), combo_row("combo 25^3", grid(img, (4, 4, 4)))]
         _emit_table(rows, os.path.join(out, "bench_crossply.csv"))
     elif suite == "fiber-desk":
-        img = ctx.generate("fiber_pack", (126,) * 3, (1.0, 1.0, 1.0), float(cfg.seed), 30, 0.03, 0.5, 0.25)
+        img = ctx.generate("fiber_pack", (126,) * 3, (1.0, 1.0, 1.0), int(cfg.seed), 30, 0.03, 0.5, 0.25)
         rows = [ref_row(img, "ref 126^3 (no combo)")]
         for fac in ((6, 6, 6), (9, 3, 3)):
             g = grid(img, fac)

@@ -135,13 +135,31 @@ def test_slab_pencil_transpose_gloo():
         assert total == single  # bitwise: chunk partials combined in global order
 
 
-def test_layout_single_rank_is_i_major():
+def test_layout_single_rank_is_j_major():
+    # one slab: rows j-major (x lines contiguous, the x + Gamma pass's order)
     from paper_2204_13624_b200 import slab_row
 
     n3p = (DIMS[2] // 2 + 1 + 7) // 8 * 8
     for c, i, j in [(0, 0, 0), (3, 5, 2), (8, 7, 5)]:
-        want = ((c * DIMS[0] + i) * DIMS[1] + j) * n3p
+        want = ((c * DIMS[1] + j) * DIMS[0] + i) * n3p
         assert slab_row(DIMS, 1, 0, 0, c, i, j) == want == slab_row(DIMS, 1, 0, 1, c, i, j)
+
+
+def test_layout_blocks_are_j_major():
+    # R slabs: block s of rank q's slab side is block q of rank s's pencil
+    # side, rows j-major inside a block
+    from paper_2204_13624_b200 import slab_row
+
+    R = 2
+    n3p = (DIMS[2] // 2 + 1 + 7) // 8 * 8
+    ni, nj = DIMS[0] // R, DIMS[1] // R
+    blk = 9 * ni * nj * n3p
+    for q in range(R):
+        for s in range(R):
+            for c, il, jl in [(0, 0, 0), (2, 1, 1), (8, ni - 1, nj - 1)]:
+                a = slab_row(DIMS, R, q, 0, c, il, s * nj + jl)
+                b = slab_row(DIMS, R, s, 1, c, q * ni + il, jl)
+                assert a - s * blk == b - q * blk == c * ni * nj * n3p + (jl * ni + il) * n3p
 
 
 def test_chunks_never_straddle_planes():

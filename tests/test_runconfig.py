@@ -103,3 +103,27 @@ def test_cli_failures_exit_nonzero_with_json(tmp_path):
     assert json.loads(r.stderr.strip().splitlines()[-1])["error"]["type"] == "ConfigInvalid"
     r = run("solve", "--out", str(tmp_path / "o"), "--override", "solver.scheme=nope")
     assert json.loads(r.stderr.strip().splitlines()[-1])["error"]["type"] == "ConfigInvalid"
+
+
+def test_fft_laplace_weights_refused():
+    # normals.conv = "fft" (normals.cpp:54-84) has no device path: refused,
+    # never silently replaced by the direct stencil
+    with pytest.raises(rc.ConfigInvalid):
+        rc.RunConfig.from_json({"normals": {"conv": "fft"}})
+    assert rc.RunConfig.from_json({"normals": {"conv": "direct"}}).to_json()["normals"]["conv"] == "direct"
+
+
+def test_cli_error_types_follow_the_reference():
+    # error_type (combo_main.cpp:395-407)
+    from paper_2204_13624_b200.__main__ import error_type
+    from paper_2204_13624_b200.combo import ComboError
+
+    assert error_type(ComboError(-1, "x")) == "ConfigInvalid"
+    assert error_type(ComboError(-2, "x")) == "InadmissibleMacroState"
+    assert error_type(ComboError(-3, "x")) == "LoadPathFailed"
+    assert error_type(ComboError(-5, "x")) == "NonDividingFactor"
+    assert error_type(ComboError(-6, "x")) == "BadShapeSpec"
+    assert error_type(ComboError(-4, "x")) == "SolverFailed"  # SingularMatrix is a combo::Error
+    for code in (-10, -11, -12, -13, -14):
+        assert error_type(ComboError(code, "x")) == "InternalError"
+    assert error_type(ValueError("x")) == "InternalError"
