@@ -148,6 +148,10 @@ typedef struct combo_step_info {
 
 /* ---------------------------------------------------------------- lifecycle */
 int combo_ctx_create(int device, combo_ctx** out);
+/* one process driving ndev GPUs: rank q of the axis-0 slab
+ * decomposition on devices[q], NCCL clique from ncclCommInitAll; bind /
+ * solve / project take and return whole-grid arrays as on one GPU. */
+int combo_ctx_create_multi(int ndev, const int* devices, combo_ctx** out);
 int combo_ctx_destroy(combo_ctx* ctx);
 const char* combo_last_error(const combo_ctx* ctx);
 const char* combo_version(void);

@@ -83,6 +83,7 @@ _VP = C.c_void_p
 # symbol -> (restype, argtypes); every function of include/combo_cuda.h
 SIGNATURES = {
     "combo_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "combo_ctx_create_multi": (C.c_int, [C.c_int, _VP, C.POINTER(C.c_void_p)]),
     "combo_ctx_destroy": (C.c_int, [_VP]),
     "combo_last_error": (C.c_char_p, [_VP]),
     "combo_version": (C.c_char_p, []),
@@ -268,12 +269,17 @@ def chunk_range(dims, nplanes, block):
 
 
 class Context:
-    """One device + stream (combo_ctx)."""
+    """One device + stream (combo_ctx); devices=[...]: one process driving
+    several GPUs as an axis-0 slab decomposition (combo_ctx_create_multi)."""
 
-    def __init__(self, device=0):
+    def __init__(self, device=0, devices=None):
         self.L = load_library()
         h = C.c_void_p()
-        self._check(self.L.combo_ctx_create(int(device), C.byref(h)), ctx=None)
+        if devices is None:
+            self._check(self.L.combo_ctx_create(int(device), C.byref(h)), ctx=None)
+        else:
+            devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+            self._check(self.L.combo_ctx_create_multi(len(devices), devs, C.byref(h)), ctx=None)
         self.h = h
 
     def close(self):

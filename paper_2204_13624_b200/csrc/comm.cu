@@ -21,6 +21,8 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -45,6 +47,8 @@ NcclApi& api() {
   a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
   a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
   a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+  a.CommAbort = reinterpret_cast<decltype(a.CommAbort)>(sym("ncclCommAbort"));
+  a.CommInitAll = reinterpret_cast<decltype(a.CommInitAll)>(sym("ncclCommInitAll"));
   a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
   a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
   a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
@@ -73,6 +77,20 @@ void nccl_init(combo_ctx* c, int nranks, int rank, const void* uid) {
   c->nccl = cm;
 }
 
+void nccl_init_all(const std::vector<combo_ctx*>& ranks) {
+  std::vector<ncclComm_t> comms(ranks.size());
+  std::vector<int> devs;
+  for (auto* r : ranks) devs.push_back(r->device);
+  ck(api().CommInitAll(comms.data(), int(ranks.size()), devs.data()), "ncclCommInitAll");
+  for (size_t k = 0; k < ranks.size(); ++k) ranks[k]->nccl = comms[k];
+}
+
+// unblocks ranks waiting in a collective after another rank failed
+void nccl_abort(combo_ctx* c) {
+  if (c->nccl) api().CommAbort(comm(c));
+  c->nccl = nullptr;
+}
+
 void nccl_destroy(combo_ctx* c) {
   if (c->nccl) api().CommDestroy(comm(c));
   c->nccl = nullptr;
@@ -89,6 +107,14 @@ void nccl_allreduce_u64(combo_ctx* c, const unsigned long long* in, unsigned lon
 
 void nccl_allreduce_sum(combo_ctx* c, double* buf, size_t n) {
   ck(api().AllReduce(buf, buf, n, ncclFloat64, ncclSum, comm(c), c->stream), "ncclAllReduce");
+}
+
+void nccl_sendrecv(combo_ctx* c, const double* send, int to, double* recv, int from, size_t count) {
+  NcclApi& a = api();
+  ck(a.GroupStart(), "ncclGroupStart");
+  ck(a.Send(send, count, ncclFloat64, to, comm(c), c->stream), "ncclSend");
+  ck(a.Recv(recv, count, ncclFloat64, from, comm(c), c->stream), "ncclRecv");
+  ck(a.GroupEnd(), "ncclGroupEnd");
 }
 
 // block s of src goes to rank s, block r of dst comes from rank r

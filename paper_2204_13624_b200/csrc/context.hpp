@@ -191,7 +191,13 @@ struct combo_ctx {
   int R = 1, q = 0;
   combo_ctx* lead = nullptr;                   // group leader (nullptr: self)
   std::vector<std::unique_ptr<combo_ctx>> vm;  // emulated ranks 1..R-1
-  void* nccl = nullptr;                        // ncclComm_t (one rank per process)
+  void* nccl = nullptr;                        // ncclComm_t (one rank per process / per peer)
+  // single-process multi-GPU (combo_ctx_create_multi): rank 0 owns the
+  // contexts of ranks 1..R-1 on the other devices; every API call runs
+  // each rank's part on a host thread of its own over the peers' NCCL clique
+  std::vector<std::unique_ptr<combo_ctx>> peers;
+  bool multi = false;     // this context owns peers
+  bool in_multi = false;  // rank of a single-process multi-GPU group (outputs are whole-grid arrays)
   bool own_stream = true;
   combo_host::DBuf<double> gpart;              // leader: block partials of all ranks
   combo_host::DBuf<combo_dev::Stats> gstats;   // NCCL: laminate stats of all ranks
@@ -213,6 +219,8 @@ struct combo_ctx {
   combo_host::DBuf<double> dfmg_warm;  // [3][8 ncomp] per doubly-fine cell of a composite host
   combo_host::DBuf<double> dfmg_pd;    // [9][8][N] per-dfc stress / tangent products
   combo_host::DBuf<double> dfmg_t8;    // [45][8 ncomp] per-dfc packed tangents
+  combo_host::DBuf<double> halo[3];    // axis-0 neighbour planes (DFMG: F above, pd below, pdir above)
+  combo_host::DBuf<double> halo_send;  // NCCL: packed boundary plane
 
   // scratch
   combo_host::DBuf<double> partials;   // per-block partial sums
@@ -257,6 +265,8 @@ inline void require_single(const combo_ctx* c) {
 }
 // comm.cu: NCCL (loaded at run time) for one-rank-per-process decompositions
 void nccl_init(combo_ctx* c, int nranks, int rank, const void* uid);
+void nccl_init_all(const std::vector<combo_ctx*>& ranks);  // ncclCommInitAll over the ranks' devices
+void nccl_abort(combo_ctx* c);
 void nccl_destroy(combo_ctx* c);
 void nccl_allgather_inplace(combo_ctx* c, double* buf, size_t count_per_rank);
 void nccl_allreduce_u64(combo_ctx* c, const unsigned long long* in, unsigned long long* out, size_t n, bool max);
@@ -272,10 +282,23 @@ void fetch_results(combo_ctx* c, bool with_stats = true);
 combo_dev::LawP law_params(const combo_law& L, double* dev_a9);
 void ensure_partials(combo_ctx* c, int64_t count);
 // dfmg.cu
-void dfmg_sweep(combo_ctx* c, const double* fin, const combo_dev::Shift9& sh, double alpha, double* out, int slot);
-void dfmg_tangent_prepare(combo_ctx* c, const double* fin, const combo_dev::Shift9& sh);
-void dfmg_matvec(combo_ctx* c, const double* fin, const combo_dev::Shift9& sh, const double* r, double* pdir,
-                 double beta, bool first, double* q);
+// (over every rank hosted by the leader c; vectors: one field per rank)
+void dfmg_sweep(combo_ctx* c, const std::vector<const double*>& fin, const combo_dev::Shift9& sh, double alpha,
+                const std::vector<double*>& out, int slot);
+void dfmg_tangent_prepare(combo_ctx* c, const std::vector<const double*>& fin, const combo_dev::Shift9& sh);
+void dfmg_matvec(combo_ctx* c, const std::vector<const double*>& fin, const combo_dev::Shift9& sh,
+                 const std::vector<const double*>& r, const std::vector<double*>& pdir, double beta, bool first,
+                 const std::vector<double*>& q);
+// engine.cu: slab-decomposition helpers
+combo_ctx* leader(combo_ctx* c);
+std::vector<combo_ctx*> members(combo_ctx* c);
+double* part_ptr(combo_ctx* c, int64_t nb, int nred);
+combo_dev::Stats* stats_ptr(combo_ctx* c);
+void group_reduce(combo_ctx* c, int64_t nb, int nred, int slot);
+combo_dev::Chunks chunks_of(const combo_ctx* c);
+int64_t chunk_blocks(const combo_ctx* c);
+// comm.cu: send count doubles to rank `to` and receive as many from `from`
+void nccl_sendrecv(combo_ctx* c, const double* send, int to, double* recv, int from, size_t count);
 
 // kernel tags for the profiler
 enum ProfTag {

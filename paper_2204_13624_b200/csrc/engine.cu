@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <sstream>
+#include <thread>
 #include <type_traits>
 
 #include "context.hpp"
@@ -415,6 +416,23 @@ void dispatch_log2(int64_t n, F&& f) {
   }
 }
 
+// COMBO_PF = waves of resident blocks a column-strip pass prefetches ahead
+// into L2 (0: off)
+int pf_waves() {
+  static const int v = [] {
+    const char* s = std::getenv("COMBO_PF");
+    return s ? std::atoi(s) : 0;
+  }();
+  return v;
+}
+template <class K>
+int ahead_blocks(const combo_ctx* c, K kernel, int threads, size_t smem) {
+  if (pf_waves() <= 0) return 0;
+  int occ = 0;
+  COMBO_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
+  return pf_waves() * std::max(occ, 1) * c->num_sms;
+}
+
 // CG matvec: bulk-staged persistent kernel (one CTA per SM) when the rows
 // are 16-byte aligned, else one cell per thread with direct loads.
 template <bool FIRST, bool HASX>
@@ -514,7 +532,7 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
       dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_rr<L, INV>;
       smem_attr(k, p.rysmem);
-      k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW);
+      k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW, ahead_blocks(c, k, p.ryT, p.rysmem));
     } else {
       dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_kernel<L, INV>;
@@ -537,7 +555,7 @@ void launch_xgamma(combo_ctx* c, int kind) {
       dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), 3u);
       auto go = [&](auto k) {
         smem_attr(k, p.rxsmem);
-        k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g);
+        k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g, ahead_blocks(c, k, p.rxT, p.rxsmem));
       };
       auto by_kind = [&](auto k0, auto k1, auto k2) {
         if (kind == 0)
@@ -608,13 +626,6 @@ void project_group(combo_ctx* c, int kind, PF&& prodf, CF&& consf, int slot_cons
   int64_t nbc = 0;
   for (size_t k = 0; k < ms.size(); ++k) nbc = launch_zinv(ms[k], consf(k));
   if (Cons::NRED) group_reduce(c, nbc, Cons::NRED, slot_cons);
-}
-
-// single-slab form (operator-level entry points, DFMG)
-template <class Prod, class Cons>
-void project_fused(combo_ctx* c, int kind, const Prod& prod, const Cons& cons, int slot_cons) {
-  if (!c->vm.empty()) throw ComboError(COMBO_ERR_STATE, "project_fused: single slab only");
-  project_group(c, kind, [&](size_t) { return prod; }, [&](size_t) { return cons; }, slot_cons);
 }
 
 void reset_stats(combo_ctx* c) {
@@ -845,10 +856,6 @@ class Solver {
       r.f = m->solver_fields;
       for (int q = 0; q < 8; ++q) r.f[q].alloc(size_t(9 * r.N));
     }
-    if (rk_.size() > 1 || c->R > 1) {
-      if (cfg.eval == COMBO_EVAL_DFMG)
-        throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: DFMG needs a single slab (axis-0 halo not implemented)");
-    }
     double lo, hi;
     const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
     spectrum_bounds(c, I, lo, hi);
@@ -866,6 +873,17 @@ class Solver {
 
  private:
   double* P(int slot, size_t k) { return rk_[k].f[slot].p; }
+  // slot `slot` of every rank
+  std::vector<double*> field(int slot) {
+    std::vector<double*> v;
+    for (size_t k = 0; k < rk_.size(); ++k) v.push_back(P(slot, k));
+    return v;
+  }
+  std::vector<const double*> cfield(int slot) {
+    std::vector<const double*> v;
+    for (size_t k = 0; k < rk_.size(); ++k) v.push_back(P(slot, k));
+    return v;
+  }
   bool run_step(const double* fbar, combo_host::StepRec& rep);
   bool run_basic(const double* fbar, combo_host::StepRec& rep);
   bool run_newton(const double* fbar, combo_host::StepRec& rep);
@@ -877,7 +895,7 @@ class Solver {
   // eval_stress (solver.cpp:59-63): per-cell sweep or DFMG; P sums -> slot
   void eval_sweep(int fin, const Shift9& sh, double alpha, int out, bool writeback, int slot) {
     if (cfg_.eval == COMBO_EVAL_DFMG) {
-      dfmg_sweep(c_, P(fin, 0), sh, alpha, P(out, 0), slot);
+      dfmg_sweep(c_, cfield(fin), sh, alpha, field(out), slot);
       return;
     }
     for (size_t k = 0; k < rk_.size(); ++k) sweep_launch(rk_[k].c, P(fin, k), sh, alpha, P(out, k), writeback);
@@ -995,7 +1013,7 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
   // dfmg_tangent_pass, solver.cpp:72-82)
   const bool dfmg = cfg_.eval == COMBO_EVAL_DFMG;
   if (dfmg)
-    dfmg_tangent_prepare(c_, P(F_, 0), shF_);
+    dfmg_tangent_prepare(c_, cfield(F_), shF_);
   else
     for (auto& r : rk_) comp_tangents(r.c, r.f[F_].p, shF_);
   int it = 0;
@@ -1020,10 +1038,10 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
     count_ls();
     ++rep.ls_cg;
     if (dfmg) {
-      dfmg_matvec(c_, P(F_, 0), shF_, P(r_, 0), P(pd_, 0), beta, it == 0, P(rb_, 0));
-      ++c_->launches;
+      dfmg_matvec(c_, cfield(F_), shF_, cfield(r_), field(pd_), beta, it == 0, field(rb_));
       COMBO_CK(cudaGetLastError());
-      project_fused(c_, cfg_.green, ProdLoad9{P(rb_, 0), rk_[0].N}, cons(0), 20);
+      project_group(
+          c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; }, cons, 20);
     } else {
       // r, F, cid, pdir (r/w), x (r/w, deferred update); composite packed tangents
       auto mv = [&](size_t k) {
@@ -1222,12 +1240,15 @@ void Solver::run(const double* fbar_target, combo_report& report) {
     backup_f[k].alloc(size_t(9 * rk_[k].N));
     if (rk_[k].c->ncomp) backup_warm[k].alloc(size_t(3 * rk_[k].c->ncomp));
   }
-  DBuf<double> dfmg_backup;  // DfmgState warm starts (solver.cpp:315,330)
+  std::vector<DBuf<double>> dfmg_backup(rk_.size());  // DfmgState warm starts (solver.cpp:315,330)
   if (cfg_.eval == COMBO_EVAL_DFMG) {
     // fresh DfmgState per solve (CellSolver ctor, solver.cpp:55)
-    c_->dfmg_warm.alloc(size_t(3 * 8 * std::max<int64_t>(c_->ncomp, 1)));
-    COMBO_CK(cudaMemsetAsync(c_->dfmg_warm.p, 0, c_->dfmg_warm.n * 8, c_->stream));
-    dfmg_backup.alloc(c_->dfmg_warm.n);
+    for (size_t k = 0; k < rk_.size(); ++k) {
+      combo_ctx* m = rk_[k].c;
+      m->dfmg_warm.alloc(size_t(3 * 8 * std::max<int64_t>(m->ncomp, 1)));
+      COMBO_CK(cudaMemsetAsync(m->dfmg_warm.p, 0, m->dfmg_warm.n * 8, m->stream));
+      dfmg_backup[k].alloc(m->dfmg_warm.n);
+    }
   }
   auto save_or_restore = [&](bool save) {
     for (size_t k = 0; k < rk_.size(); ++k) {
@@ -1238,10 +1259,10 @@ void Solver::run(const double* fbar_target, combo_report& report) {
       if (m->ncomp)
         COMBO_CK(cudaMemcpyAsync(save ? backup_warm[k].p : m->warm.p, save ? m->warm.p : backup_warm[k].p,
                                  size_t(3 * m->ncomp) * sizeof(double), cudaMemcpyDeviceToDevice, m->stream));
+      if (dfmg_backup[k].p)
+        COMBO_CK(cudaMemcpyAsync(save ? dfmg_backup[k].p : m->dfmg_warm.p, save ? m->dfmg_warm.p : dfmg_backup[k].p,
+                                 dfmg_backup[k].n * sizeof(double), cudaMemcpyDeviceToDevice, m->stream));
     }
-    if (dfmg_backup.p)
-      COMBO_CK(cudaMemcpyAsync(save ? dfmg_backup.p : c_->dfmg_warm.p, save ? c_->dfmg_warm.p : dfmg_backup.p,
-                               dfmg_backup.n * sizeof(double), cudaMemcpyDeviceToDevice, c_->stream));
   };
   try {
     while (t < 1.0 - 1e-12) {
@@ -1308,7 +1329,7 @@ void Solver::final_stress(const std::vector<double*>& out) {
   const Shift9 sh = last_eval_ >= 0 ? last_eval_shift_ : shF_;
   reset_stats(c_);
   if (cfg_.eval == COMBO_EVAL_DFMG) {
-    dfmg_sweep(c_, P(fin, 0), sh, 0.0, out[0], 40);
+    dfmg_sweep(c_, cfield(fin), sh, 0.0, out, 40);
     return;
   }
   for (size_t k = 0; k < rk_.size(); ++k) sweep_launch(rk_[k].c, P(fin, k), sh, 0.0, out[k], false);
@@ -1375,6 +1396,41 @@ int guarded(combo_ctx* c, Fn&& fn) {
   }
 }
 
+// Every rank of a single-process multi-GPU group runs fn on its own host
+// thread with its device current (the NCCL clique needs all ranks inside a
+// collective at once); a plain context runs fn inline. A failing rank
+// aborts the clique so the others leave their collectives, and the first
+// error is rethrown.
+template <class Fn>
+void on_ranks(combo_ctx* c, Fn&& fn) {
+  if (!c->multi) {
+    fn(c);
+    return;
+  }
+  std::vector<combo_ctx*> rs{c};
+  for (auto& p : c->peers) rs.push_back(p.get());
+  std::vector<std::exception_ptr> errs(rs.size());
+  std::vector<std::thread> th;
+  for (size_t k = 0; k < rs.size(); ++k)
+    th.emplace_back([&, k] {
+      try {
+        COMBO_CK(cudaSetDevice(rs[k]->device));
+        fn(rs[k]);
+      } catch (...) {
+        errs[k] = std::current_exception();
+        for (auto* r : rs) {
+          try {
+            nccl_abort(r);
+          } catch (...) {
+          }
+        }
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
 void require_bound(const combo_ctx* c) {
   if (!c->bound) throw ComboError(COMBO_ERR_STATE, "materials not bound (combo_bind_materials)");
 }
@@ -1424,8 +1480,48 @@ int combo_ctx_create(int device, combo_ctx** out) {
   return COMBO_OK;
 }
 
+// One process, R GPUs (combo_ctx_create(ndev, devices)):
+// rank q lives on devices[q], the slab / pencil exchanges and reductions run
+// over an ncclCommInitAll clique; bind / solve / project take whole-grid
+// arrays as with one GPU.
+int combo_ctx_create_multi(int ndev, const int* devices, combo_ctx** out) {
+  if (!out || ndev < 1 || !devices) return COMBO_ERR_BAD_ARGUMENT;
+  *out = nullptr;
+  for (int a = 0; a < ndev; ++a)
+    for (int b = a + 1; b < ndev; ++b)
+      if (devices[a] == devices[b]) return COMBO_ERR_BAD_ARGUMENT;
+  combo_ctx* lead = nullptr;
+  int rc = combo_ctx_create(devices[0], &lead);
+  if (rc) return rc;
+  rc = guarded(lead, [&] {
+    std::vector<combo_ctx*> rs{lead};
+    for (int q = 1; q < ndev; ++q) {
+      combo_ctx* p = nullptr;
+      const int r = combo_ctx_create(devices[q], &p);
+      if (r) throw ComboError(r, "combo_ctx_create_multi: device " + std::to_string(devices[q]));
+      lead->peers.emplace_back(p);
+      rs.push_back(p);
+    }
+    if (ndev > 1) nccl_init_all(rs);  // one device: the same threaded path without a clique
+    for (int q = 0; q < ndev; ++q) {
+      rs[size_t(q)]->R = ndev;
+      rs[size_t(q)]->q = q;
+      rs[size_t(q)]->in_multi = true;
+    }
+    lead->multi = true;
+  });
+  if (rc) {
+    combo_ctx_destroy(lead);
+    return rc;
+  }
+  *out = lead;
+  return COMBO_OK;
+}
+
 int combo_ctx_destroy(combo_ctx* c) {
   if (!c) return COMBO_OK;
+  for (auto& p : c->peers) combo_ctx_destroy(p.release());
+  c->peers.clear();
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& m : c->vm)
@@ -1447,11 +1543,12 @@ const char* combo_last_error(const combo_ctx* c) { return c ? c->err.c_str() : "
 int combo_kernel_launches(const combo_ctx* c, int64_t* count) {
   if (!c || !count) return COMBO_ERR_BAD_ARGUMENT;
   *count = c->launches;
+  for (const auto& p : c->peers) *count += p->launches;
   return COMBO_OK;
 }
 
 int combo_synchronize(combo_ctx* c) {
-  return guarded(c, [&] { COMBO_CK(cudaStreamSynchronize(c->stream)); });
+  return guarded(c, [&] { on_ranks(c, [](combo_ctx* r) { COMBO_CK(cudaStreamSynchronize(r->stream)); }); });
 }
 
 int combo_profile_enable(combo_ctx* c, int enable) {
@@ -1498,7 +1595,9 @@ const char* combo_profile_json(combo_ctx* c) {
 
 int combo_set_grid(combo_ctx* c, const int64_t dims[3], const double lengths[3]) {
   return guarded(c, [&] {
-    for (combo_ctx* m : members(c)) set_grid(m, dims, lengths);
+    on_ranks(c, [&](combo_ctx* r) {
+      for (combo_ctx* m : members(r)) set_grid(m, dims, lengths);
+    });
   });
 }
 
@@ -1509,7 +1608,7 @@ int combo_set_grid(combo_ctx* c, const int64_t dims[3], const double lengths[3])
 int combo_ctx_set_virtual_ranks(combo_ctx* c, int nranks) {
   return guarded(c, [&] {
     if (nranks < 1) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "nranks must be >= 1");
-    if (c->nccl) throw ComboError(COMBO_ERR_STATE, "context already joined an NCCL decomposition");
+    if (c->nccl || c->in_multi) throw ComboError(COMBO_ERR_STATE, "context already joined an NCCL decomposition");
     COMBO_CK(cudaStreamSynchronize(c->stream));
     c->vm.clear();
     c->R = nranks;
@@ -1542,6 +1641,7 @@ int combo_ctx_set_ranks(combo_ctx* c, int nranks, int rank, const void* nccl_id)
   return guarded(c, [&] {
     if (nranks < 1 || rank < 0 || rank >= nranks) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "bad rank / nranks");
     if (!c->vm.empty()) throw ComboError(COMBO_ERR_STATE, "context hosts emulated ranks");
+    if (c->in_multi) throw ComboError(COMBO_ERR_STATE, "context is a multi-GPU group (combo_ctx_create_multi)");
     if (nranks > 1 && !nccl_id) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "nccl_id required for nranks > 1");
     nccl_destroy(c);
     c->R = nranks;
@@ -1602,7 +1702,7 @@ int combo_ctx_ranks(const combo_ctx* c, int* nranks, int* rank, int* local_ranks
   if (!c) return COMBO_ERR_BAD_ARGUMENT;
   if (nranks) *nranks = c->R;
   if (rank) *rank = c->q;
-  if (local_ranks) *local_ranks = int(1 + c->vm.size());
+  if (local_ranks) *local_ranks = int(1 + c->vm.size() + c->peers.size());
   const int64_t n = c->has_grid ? c->dims[0] / c->R : 0;
   if (i0) *i0 = int64_t(c->q) * n;
   if (ni) *ni = n;
@@ -1675,13 +1775,17 @@ int bind_members(combo_ctx* c, const int64_t dims[3], const double lengths[3], c
                  int combo, const combo_laminate_opts* lam, int mem, bool local) {
   return guarded(c, [&] {
     if (!kind || !c_plus || !matrix || !inclusion) throw ComboError(COMBO_ERR_BAD_ARGUMENT, "null argument");
-    for (combo_ctx* m : members(c)) {
-      m->R = c->R;
-      set_grid(m, dims, lengths);
-      const int64_t off = int64_t(local ? m->q - c->q : m->q) * m->N;
-      bind_slab(m, dims, lengths, kind + off, c_plus + off, normal3 ? normal3 + 3 * off : nullptr, matrix, inclusion,
-                combo, lam, mem);
-    }
+    // a multi-GPU group's local slabs are the whole grid
+    const int q0 = local && !c->multi ? c->q : 0;
+    on_ranks(c, [&](combo_ctx* r) {
+      for (combo_ctx* m : members(r)) {
+        m->R = r->R;
+        set_grid(m, dims, lengths);
+        const int64_t off = int64_t(m->q - q0) * m->N;
+        bind_slab(m, dims, lengths, kind + off, c_plus + off, normal3 ? normal3 + 3 * off : nullptr, matrix,
+                  inclusion, combo, lam, mem);
+      }
+    });
     ++c->bind_gen;
   });
 }
@@ -1710,8 +1814,9 @@ int combo_bind_generation(const combo_ctx* c, int64_t* gen) {
 
 int combo_composite_cells(const combo_ctx* c, int64_t* count) {
   if (!c || !count) return COMBO_ERR_BAD_ARGUMENT;
-  *count = c->ncomp;  // emulated ranks: all slabs; one rank per process: this slab
+  *count = c->ncomp;  // emulated ranks / multi-GPU group: all slabs; one rank per process: this slab
   for (const auto& m : c->vm) *count += m->ncomp;
+  for (const auto& m : c->peers) *count += m->ncomp;
   return COMBO_OK;
 }
 
@@ -1767,11 +1872,13 @@ int combo_set_warm_starts(combo_ctx* c, const double* warm3, int mem) {
 int combo_reset_warm_starts(combo_ctx* c) {
   return guarded(c, [&] {
     require_bound(c);
-    for (combo_ctx* m : members(c)) {
-      if (m->ncomp) COMBO_CK(cudaMemsetAsync(m->warm.p, 0, size_t(3 * m->ncomp) * 8, m->stream));
-      if (m->dfmg_warm.p) COMBO_CK(cudaMemsetAsync(m->dfmg_warm.p, 0, m->dfmg_warm.n * 8, m->stream));
-    }
-    COMBO_CK(cudaStreamSynchronize(c->stream));
+    on_ranks(c, [](combo_ctx* r) {
+      for (combo_ctx* m : members(r)) {
+        if (m->ncomp) COMBO_CK(cudaMemsetAsync(m->warm.p, 0, size_t(3 * m->ncomp) * 8, m->stream));
+        if (m->dfmg_warm.p) COMBO_CK(cudaMemsetAsync(m->dfmg_warm.p, 0, m->dfmg_warm.n * 8, m->stream));
+      }
+      COMBO_CK(cudaStreamSynchronize(r->stream));
+    });
   });
 }
 
@@ -1949,29 +2056,46 @@ int combo_tangent45_matvec(combo_ctx* c, const double* t45, const double* x, dou
   });
 }
 
+// whole-grid [9][N] arrays <-> the slabs: slab k of rank r's members is
+// rows [(r0 + k) Nl, ...) of every component, r0 = the multi-GPU rank
+// (members of emulated ranks and single contexts: 0)
+namespace {
+struct SlabRows {
+  int64_t Nl, Nt, r0;
+};
+SlabRows slab_rows(combo_ctx* r) {
+  const int64_t nloc = int64_t(members(r).size());
+  const int64_t R = r->in_multi ? r->R : nloc;
+  return SlabRows{r->N, r->N * R, r->in_multi ? r->q : 0};
+}
+}  // namespace
+
 int combo_project(combo_ctx* c, int kind, const double* in, double* out, int mem) {
   return guarded(c, [&] {
     if (!c->has_grid) throw ComboError(COMBO_ERR_STATE, "no grid (combo_set_grid)");
-    ensure_scratch(c);
-    // in / out: [9][N] of the grid (emulated ranks: split into / gathered
-    // from the slabs; one rank per process: this rank's slab)
-    const auto ms = members(c);
-    const int64_t Nl = c->N, Nt = Nl * int64_t(ms.size());
-    const auto h2d = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    const auto d2h = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    for (size_t k = 0; k < ms.size(); ++k) {
-      ms[k]->scratch[0].alloc(size_t(9 * Nl));
-      ms[k]->scratch[1].alloc(size_t(9 * Nl));
-      COMBO_CK(cudaMemcpy2DAsync(ms[k]->scratch[0].p, size_t(Nl) * 8, in + int64_t(k) * Nl, size_t(Nt) * 8,
-                                 size_t(Nl) * 8, 9, h2d, c->stream));
-    }
-    project_group(
-        c, kind, [&](size_t k) { return ProdLoad9{ms[k]->scratch[0].p, Nl}; },
-        [&](size_t k) { return ConsStore9{ms[k]->scratch[1].p, Nl}; }, 0);
-    for (size_t k = 0; k < ms.size(); ++k)
-      COMBO_CK(cudaMemcpy2DAsync(out + int64_t(k) * Nl, size_t(Nt) * 8, ms[k]->scratch[1].p, size_t(Nl) * 8,
-                                 size_t(Nl) * 8, 9, d2h, c->stream));
-    COMBO_CK(cudaStreamSynchronize(c->stream));
+    // in / out: [9][N] of the grid (emulated ranks / multi-GPU group: split
+    // into / gathered from the slabs; one rank per process: this rank's slab)
+    on_ranks(c, [&](combo_ctx* r) {
+      ensure_scratch(r);
+      const auto ms = members(r);
+      const SlabRows sr = slab_rows(r);
+      const int64_t Nl = sr.Nl;
+      const auto h2d = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+      const auto d2h = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+      for (size_t k = 0; k < ms.size(); ++k) {
+        ms[k]->scratch[0].alloc(size_t(9 * Nl));
+        ms[k]->scratch[1].alloc(size_t(9 * Nl));
+        COMBO_CK(cudaMemcpy2DAsync(ms[k]->scratch[0].p, size_t(Nl) * 8, in + (sr.r0 + int64_t(k)) * Nl,
+                                   size_t(sr.Nt) * 8, size_t(Nl) * 8, 9, h2d, r->stream));
+      }
+      project_group(
+          r, kind, [&](size_t k) { return ProdLoad9{ms[k]->scratch[0].p, Nl}; },
+          [&](size_t k) { return ConsStore9{ms[k]->scratch[1].p, Nl}; }, 0);
+      for (size_t k = 0; k < ms.size(); ++k)
+        COMBO_CK(cudaMemcpy2DAsync(out + (sr.r0 + int64_t(k)) * Nl, size_t(sr.Nt) * 8, ms[k]->scratch[1].p,
+                                   size_t(Nl) * 8, size_t(Nl) * 8, 9, d2h, r->stream));
+      COMBO_CK(cudaStreamSynchronize(r->stream));
+    });
   });
 }
 
@@ -2019,32 +2143,37 @@ int combo_solve(combo_ctx* c, const double fbar[9], const combo_solver_cfg* cfg,
       throw ComboError(COMBO_ERR_CONFIG_INVALID, "solver: tol_equilibrium must be positive");
     if (!(hdet3(fbar) > 0.0)) throw ComboError(COMBO_ERR_INADMISSIBLE_MACRO, "solve: det(fbar) <= 0");
     auto rep = std::make_unique<combo_report>();
-    Solver s(c, *cfg);
-    s.run(fbar, *rep);
-    if (pbar) std::memcpy(pbar, s.pbar(), 9 * sizeof(double));
-    // outputs: [9][N] of the grid (emulated ranks gathered in slab order);
-    // with one rank per process, this rank's slab [9][N_local]
-    const auto ms = members(c);
-    auto gather = [&](double* out, std::vector<double*> src) {
-      const int64_t Nl = c->N, Nt = Nl * int64_t(ms.size());
-      const auto kind = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-      for (size_t k = 0; k < src.size(); ++k)
-        COMBO_CK(cudaMemcpy2DAsync(out + int64_t(k) * Nl, size_t(Nt) * 8, src[k], size_t(Nl) * 8, size_t(Nl) * 8, 9,
-                                   kind, c->stream));
-    };
-    if (P_out) {
-      std::vector<double*> p;
-      for (size_t k = 0; k < s.nranks(); ++k) p.push_back(s.scratch(k));
-      s.final_stress(p);
-      gather(P_out, p);
-    }
-    if (F_out) {
-      s.materialize();
-      std::vector<double*> f;
-      for (size_t k = 0; k < s.nranks(); ++k) f.push_back(s.F(k));
-      gather(F_out, f);
-    }
-    COMBO_CK(cudaStreamSynchronize(c->stream));
+    on_ranks(c, [&](combo_ctx* r) {
+      auto rr = std::make_unique<combo_report>();
+      Solver s(r, *cfg);
+      s.run(fbar, *rr);
+      // outputs: [9][N] of the grid (emulated ranks / multi-GPU group
+      // gathered in slab order); with one rank per process, its slab
+      const SlabRows sr = slab_rows(r);
+      auto gather = [&](double* out, std::vector<double*> src) {
+        const auto kind = mem == COMBO_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        for (size_t k = 0; k < src.size(); ++k)
+          COMBO_CK(cudaMemcpy2DAsync(out + (sr.r0 + int64_t(k)) * sr.Nl, size_t(sr.Nt) * 8, src[k],
+                                     size_t(sr.Nl) * 8, size_t(sr.Nl) * 8, 9, kind, r->stream));
+      };
+      if (P_out) {
+        std::vector<double*> p;
+        for (size_t k = 0; k < s.nranks(); ++k) p.push_back(s.scratch(k));
+        s.final_stress(p);
+        gather(P_out, p);
+      }
+      if (F_out) {
+        s.materialize();
+        std::vector<double*> f;
+        for (size_t k = 0; k < s.nranks(); ++k) f.push_back(s.F(k));
+        gather(F_out, f);
+      }
+      COMBO_CK(cudaStreamSynchronize(r->stream));
+      if (r == c) {  // every rank holds the same report and P-bar
+        if (pbar) std::memcpy(pbar, s.pbar(), 9 * sizeof(double));
+        rep = std::move(rr);
+      }
+    });
     rep->json = report_json(*rep);
     if (report)
       *report = rep.release();

@@ -158,6 +158,27 @@ __device__ __forceinline__ int rr_first_pos(int u, int i) {
 // padded element index (one spare slot per 8 elements)
 __device__ __forceinline__ int pad8(int e) { return e + (e >> 3); }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Wave-ahead L2 prefetch of a column-strip tile: the block `ahead` launch
+// positions after this one (about one wave of resident blocks later) gets
+// its rows into L2 now, so its loads see L2 instead of DRAM latency. The
+// grid is (column blocks, lines, channel groups); rows(b1, b2, t) gives the
+// address of the t-th row segment of block (x = b0, y = b1, z = b2).
+template <class Rows>
+__device__ __forceinline__ void prefetch_ahead(int ahead, int nrows, const Rows& rows) {
+  if (ahead <= 0) return;
+  const int64_t nb = int64_t(gridDim.x) * gridDim.y * gridDim.z;
+  const int64_t b = blockIdx.x + int64_t(gridDim.x) * (blockIdx.y + int64_t(gridDim.y) * blockIdx.z) + ahead;
+  if (b >= nb) return;
+  const int b0 = int(b % gridDim.x);
+  const int64_t r = b / gridDim.x;
+  const int b1 = int(r % gridDim.y), b2 = int(r / gridDim.y);
+  for (int t = threadIdx.x; t < nrows; t += blockDim.x) prefetch_l2(rows(b0, b1, b2, t));
+}
+
 // ---------------------------------------------------------------- reductions
 // Threads are grouped in power-of-two groups of G lanes sharing the same
 // (component a, component b) pair; per group: NSC scalars, plus per-component
@@ -410,9 +431,12 @@ static __global__ void __launch_bounds__(512, 2)
 // one tile: columns [kc0, kc0 + W) of component c, local plane i
 template <int L, bool INV, bool CG = false>
 __device__ __forceinline__ void ypass_tile(const SpecView& sv, const double2* __restrict__ tw, int W, int c,
-                                           int64_t i, int kc0) {
+                                           int64_t i, int kc0, int ahead = 0) {
   constexpr int N = 1 << L;
   extern __shared__ double2 sm[];
+  prefetch_ahead(ahead, N, [&](int b0, int b1, int b2, int t) {
+    return sv.spec + int64_t(b2) * sv.cs + b0 * W + sv.rowA(b1, t);
+  });
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
@@ -434,8 +458,9 @@ __device__ __forceinline__ void ypass_tile(const SpecView& sv, const double2* __
 }
 
 template <int L, bool INV, int MAXT = 512, int MINB = 2>
-static __global__ void __launch_bounds__(MAXT, MINB) ypass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
-  ypass_tile<L, INV>(sv, tw, W, blockIdx.z, blockIdx.y, blockIdx.x * W);
+static __global__ void __launch_bounds__(MAXT, MINB)
+    ypass_rr(SpecView sv, const double2* __restrict__ tw, int W, int ahead) {
+  ypass_tile<L, INV>(sv, tw, W, blockIdx.z, blockIdx.y, blockIdx.x * W, ahead);
 }
 
 // ---------------------------------------------------------------- X + Gamma
@@ -535,7 +560,7 @@ __device__ __forceinline__ void rank_gamma(const GreenTables& G, const RankCol<K
 
 template <int L, int KIND, int MAXT, int MINB>
 static __global__ void __launch_bounds__(MAXT, MINB)
-    xgamma_v4(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G) {
+    xgamma_v4(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G, int ahead) {
   constexpr int N = 1 << L;
   extern __shared__ double2 sm[];
   const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
@@ -543,6 +568,9 @@ static __global__ void __launch_bounds__(MAXT, MINB)
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
   const int64_t plane = sv.cs;
+  prefetch_ahead(ahead, 3 * N, [&](int b0, int b1, int b2, int t) {
+    return sv.spec + int64_t(3 * b2 + t / N) * plane + b0 * W + sv.rowB(t % N, b1);
+  });
   double2* base = sv.spec + int64_t(3 * rg) * plane + kc0 + line;  // pencil side, local k2 j
   const RankCol<KIND> col = rank_col<KIND>(G, rg, sv.j0 + j, kc0 + line, sv.n2, sv.n3);
   double2 v[2][8];

@@ -100,3 +100,55 @@ def test_rank_shape_errors(fresh):
     c2.set_grid((8, 8, 8))
     with pytest.raises(ComboError):
         c2.fft_forward((8, 8, 8), np.zeros((9, 8, 8, 8)))  # operator-level entry points: one slab
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_dfmg_solve_rank_invariant(fresh, oracle, R):
+    """DFMG on R slabs: one-plane axis-0 halos of F / pdir (gather_dfc reads
+    i + 1) and of the per-dfc stresses (the assembly reads i - 1,
+    dfmg.cpp:27-47, 148-156); bitwise equal to one slab, which matches the
+    oracle"""
+    soft, stiff = neo_hookean_enu(1.0, 0.0), neo_hookean_enu(10.0, 0.3)
+    base = fresh(1)
+    img = base.generate("boolean_ellipsoids", (32, 32, 32), (1, 1, 1), 3, 2.0, 4.0, 0.25)
+    kind, cp, _ = base.coarsen(img, (2, 2, 2))
+    n, _, _ = base.compute_normals(img, (2, 2, 2), kind)
+    kw = dict(green="staggered", eval="dfmg", tol_equilibrium=1e-8, load_steps=2)
+    r1 = CellMaterials(base, (16, 16, 16), kind, cp, n, soft, stiff).solve(shear(0.3), **kw)
+    assert r1["report"]["success"]
+    rr = CellMaterials(fresh(R), (16, 16, 16), kind, cp, n, soft, stiff).solve(shear(0.3), **kw)
+    assert np.array_equal(rr["pbar"], r1["pbar"]) and np.array_equal(rr["f"], r1["f"])
+    assert np.array_equal(rr["p"], r1["p"])
+    for s1, s2 in zip(r1["report"]["steps"], rr["report"]["steps"]):
+        assert s1["cg_iters"] == s2["cg_iters"] and s1["residuals"] == s2["residuals"]
+    cmo = oracle.CellMaterials((16, 16, 16), kind, cp, n, oracle.neo_hookean_enu(1.0, 0.0),
+                               oracle.neo_hookean_enu(10.0, 0.3))
+    ro = cmo.solve(shear(0.3), scheme=1, green=2, eval=1, tol=1e-8, load_steps=2)
+    assert np.linalg.norm(rr["pbar"] - ro["pbar"]) <= 1e-9 * np.linalg.norm(ro["pbar"])
+
+
+def test_multi_gpu_context_single_device(oracle):
+    """combo_ctx_create_multi (one process, R GPUs, ranks on host threads):
+    with the one GPU available the same threaded path runs one rank; the
+    solve equals the plain context's bit for bit (a clique of R > 1 GPUs
+    needs as many devices)"""
+    import torch
+
+    soft, stiff = neo_hookean_enu(1.0, 0.0), neo_hookean_enu(10.0, 0.3)
+    plain = Context(0)
+    kind, cp, n = _sphere_problem(plain)
+    kw = dict(tol_equilibrium=1e-8, load_steps=2)
+    r1 = CellMaterials(plain, (16, 16, 16), kind, cp, n, soft, stiff).solve(shear(0.4), **kw)
+    multi = Context(devices=[0])
+    assert multi.ranks()["nranks"] == 1
+    r2 = CellMaterials(multi, (16, 16, 16), kind, cp, n, soft, stiff).solve(shear(0.4), **kw)
+    assert np.array_equal(r1["f"], r2["f"]) and np.array_equal(r1["pbar"], r2["pbar"])
+    tau = np.random.default_rng(3).uniform(-1, 1, 9 * 512)
+    assert np.array_equal(multi.project(tau, "rotated", (8, 8, 8)), plain.project(tau, "rotated", (8, 8, 8)))
+    if torch.cuda.device_count() > 1:
+        m2 = Context(devices=[0, 1])
+        r3 = CellMaterials(m2, (16, 16, 16), kind, cp, n, soft, stiff).solve(shear(0.4), **kw)
+        assert np.array_equal(r1["f"], r3["f"]) and np.array_equal(r1["pbar"], r3["pbar"])
+        m2.close()
+    multi.close()
+    plain.close()

@@ -310,3 +310,16 @@ def test_lean_tangent_storage_bitwise(oracle, monkeypatch):
     assert a["report"]["error"] == "LsBudgetExhausted" and len(a["report"]["steps"]) == 1
     assert a["report"]["steps"][0]["residuals"] == b["report"]["steps"][0]["residuals"]
     assert np.array_equal(a["f"].view(np.uint64), b["f"].view(np.uint64))
+
+
+def test_c8_scheme_cross_agreement_fixture():
+    """Acceptance criterion 8 (acceptance.cpp:321-404): the oracle's four
+    scheme runs on the 32^3 combo sphere reproduce the pairwise deviations
+    of the reference's recorded run to the printed digits
+    (test_output.txt:40-45; tools/oracle_c8.py wrote the fixture). This pins
+    the basic scheme and staggered + DFMG end to end."""
+    import json
+    import os
+
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c8_oracle.json")))
+    assert [round(x, 3) for x in d["deviation_percent"]] == d["recorded_percent"]
