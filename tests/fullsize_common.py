@@ -22,7 +22,7 @@ CASES = {
     "C3": dict(config="C3", first_increment=False, max_ls=0),
     "C4": dict(config="C4", first_increment=False, max_ls=70),
     # the bench workload itself (bench.py: C5 1-GPU variant, first increment)
-    "C5": dict(config="C5", first_increment=True, max_ls=0),
+    "C5": dict(config="C5", first_increment=True, max_ls=90),
 }
 
 N_SAMPLE = 1024  # uniform sample cells (+ as many composite cells)
