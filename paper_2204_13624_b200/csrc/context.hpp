@@ -1,6 +1,7 @@
 // Host-side context of the B200 ComBo engine (one device, one stream).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <array>
@@ -109,6 +110,11 @@ struct FftPlan {
   bool mv_bulk = true;  // bulk-staged CG matvec (COMBO_MV_BULK=0: one cell per thread, direct loads)
   bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
+  // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
+  // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off
+  bool tma_x = false, tma_y = false;
+  int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
+  CUtensorMap xmap{}, ymap{};
   // slab decomposition (R ranks, this plan's rank q): planes [i0, i0 + ni)
   // on the slab side, k2 in [j0, j0 + nj) on the pencil side
   int R = 1, q = 0;

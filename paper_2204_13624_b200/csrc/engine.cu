@@ -15,6 +15,7 @@
 #include <type_traits>
 
 #include "context.hpp"
+#include "fft_tma.cuh"
 
 using namespace combo_dev;
 
@@ -134,6 +135,52 @@ void ensure_scratch(combo_ctx* c) {
   }
 }
 
+// 4-D tensor map over the single-slab spectrum for the TMA-staged strip
+// passes (fft_tma.cuh): coordinates (column in doubles, row index with the
+// smaller stride, the other row index, component); the box spans W columns
+// and up to 256 rows of the transformed index.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    COMBO_CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess)
+      throw ComboError(COMBO_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// returns lineFirst (the transformed index is coordinate 1)
+int encode_strip_map(CUtensorMap* m, const FftPlan& p, bool xpass, int W) {
+  const combo_dev::SpecView sv = p.sv();
+  const bool i_first = sv.si < sv.sj;
+  const int64_t n1 = p.dims[0], n2 = p.dims[1];
+  const cuuint64_t gdim[4] = {cuuint64_t(2 * p.n3p), cuuint64_t(i_first ? n1 : n2), cuuint64_t(i_first ? n2 : n1), 9};
+  const cuuint64_t gstr[3] = {cuuint64_t(16 * std::min(sv.si, sv.sj)), cuuint64_t(16 * std::max(sv.si, sv.sj)),
+                              cuuint64_t(16 * sv.cs)};
+  const bool line_first = xpass == i_first;
+  const int64_t n = xpass ? n1 : n2;
+  const cuuint32_t rb = cuuint32_t(std::min<int64_t>(n, 256));
+  const cuuint32_t box[4] = {cuuint32_t(2 * W), line_first ? rb : 1u, line_first ? 1u : rb, xpass ? 3u : 1u};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = encode_tiled_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, p.spec.p, gdim, gstr, box, es,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw ComboError(COMBO_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return line_first ? 1 : 0;
+}
+
+bool pow2_between(int64_t n, int lo, int hi) {
+  for (int l = lo; l <= hi; ++l)
+    if (n == (int64_t(1) << l)) return true;
+  return false;
+}
+
 void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   for (int a = 0; a < 3; ++a) {
     if (dims[a] < 1) throw ComboError(COMBO_ERR_BAD_SHAPE, "grid dims must be >= 1");
@@ -243,6 +290,20 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->spec.alloc(size_t(9 * p->ni * d[1] * p->n3p));
   if (R > 1) {
     p->specB.alloc(size_t(9 * p->ni * d[1] * p->n3p));
+  }
+  // TMA-staged strip passes: single slab, lines of 64..1024 points
+  if (R == 1 && p->n3c >= 8) {
+    if (knob("COMBO_XTMA", 1) != 0 && pow2_between(d[0], 6, 10)) {
+      p->tma_x_line_first = encode_strip_map(&p->xmap, *p, true, combo_dev::kTmaW);
+      p->tma_x = true;
+    }
+    if (knob("COMBO_YTMA", 1) != 0 && pow2_between(d[1], 6, 10)) {
+      p->tma_yw = d[1] >= 1024 ? 4 : 8;
+      if (d[1] < 1024 && (knob("COMBO_YTMA_W", 0) == 4 || knob("COMBO_YTMA_W", 0) == 8))
+        p->tma_yw = knob("COMBO_YTMA_W", 0);
+      p->tma_y_line_first = encode_strip_map(&p->ymap, *p, false, p->tma_yw);
+      p->tma_y = true;
+    }
   }
   c->plan = std::move(p);
 }
@@ -528,6 +589,22 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
   ProfScope ps(c, INV ? kTagYinv : kTagYfwd, 2.0 * spec_bytes(c) * ncomp / 9.0);
   dispatch_log2(p.dims[1], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
+    if constexpr (L >= 6) {
+      if (p.tma_y) {
+        auto go = [&](auto k, int W) {
+          const size_t smem = size_t((p.dims[1] + p.dims[1] / 8) * W) * sizeof(double2);
+          dim3 grid(unsigned((p.n3c + W - 1) / W), unsigned(p.ni), unsigned(ncomp));
+          smem_attr(k, smem);
+          k<<<grid, int(p.dims[1] / 8) * W, smem, c->stream>>>(p.ymap, p.sv(), p.ax[1].tw.p, p.tma_y_line_first);
+        };
+        if (p.tma_yw == 8) {
+          if constexpr (L <= 9) go(ypass_tma<L, INV, 8>, 8);
+        } else {
+          go(ypass_tma<L, INV, 4>, 4);
+        }
+        return;
+      }
+    }
     if constexpr (L >= 3) {
       dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_rr<L, INV>;
@@ -550,6 +627,24 @@ void launch_xgamma(combo_ctx* c, int kind) {
   ProfScope ps(c, kTagXGamma, 2.0 * spec_bytes(c));
   dispatch_log2(p.dims[0], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
+    if constexpr (L >= 6) {
+      if (p.tma_x) {
+        constexpr int W = combo_dev::kTmaW;
+        const size_t smem = size_t(3 * p.dims[0] * W) * sizeof(double2);
+        dim3 grid(unsigned((p.n3c + W - 1) / W), unsigned(p.nj), 3u);
+        auto go = [&](auto k) {
+          smem_attr(k, smem);
+          k<<<grid, int(p.dims[0] / 8) * W, smem, c->stream>>>(p.xmap, p.svB(), p.ax[0].tw.p, g, p.tma_x_line_first);
+        };
+        if (kind == 0)
+          go(xgamma_tma<L, 0>);
+        else if (kind == 1)
+          go(xgamma_tma<L, 1>);
+        else
+          go(xgamma_tma<L, 2>);
+        return;
+      }
+    }
     if constexpr (L >= 3) {
       // rank-1 x + Gamma (fft_rr.cuh): two channels per thread
       dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), 3u);
