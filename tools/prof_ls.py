@@ -9,7 +9,7 @@ import numpy as np  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2204_13624_b200 import CellMaterials, Context, neo_hookean  # noqa: E402
-from paper_2204_13624_b200.configs import CONFIGS, scaled  # noqa: E402
+from paper_2204_13624_b200.configs import CONFIGS, build_slab_grid, scaled  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5")
@@ -18,7 +18,7 @@ ap.add_argument("--ls", type=int, default=4)
 a = ap.parse_args()
 cfg = scaled(CONFIGS[a.config], a.scale)
 ctx = Context(0)
-kind, cp, nrm, _ = bench.build_problem_gpu(ctx, cfg)
+kind, cp, nrm, _ = build_slab_grid(ctx, cfg)
 cm = CellMaterials(ctx, cfg.grid, kind, cp, nrm, neo_hookean(*cfg.matrix), neo_hookean(*cfg.inclusion))
 r = cm.solve(bench.first_increment(cfg), want_fields=False, scheme=cfg.scheme, green=cfg.green,
              tol_equilibrium=cfg.tol, load_steps=1, max_ls_iterations=a.ls)
