@@ -117,17 +117,19 @@ void nccl_sendrecv(combo_ctx* c, const double* send, int to, double* recv, int f
   ck(a.GroupEnd(), "ncclGroupEnd");
 }
 
-// block s of src goes to rank s, block r of dst comes from rank r
-void nccl_alltoall_blocks(combo_ctx* c, const double2* src, double2* dst, size_t blk) {
+// elements [off, off + cnt) of block s of src go to rank s, the same range of
+// block r of dst comes from rank r (blocks of blk elements)
+void nccl_alltoall_blocks(combo_ctx* c, const double2* src, double2* dst, size_t blk, size_t off, size_t cnt,
+                          cudaStream_t stream) {
   NcclApi& a = api();
-  const size_t n = 2 * blk;  // doubles per block
-  COMBO_CK(cudaMemcpyAsync(dst + size_t(c->q) * blk, src + size_t(c->q) * blk, blk * sizeof(double2),
-                           cudaMemcpyDeviceToDevice, c->stream));
+  const size_t n = 2 * cnt;  // doubles per message
+  COMBO_CK(cudaMemcpyAsync(dst + size_t(c->q) * blk + off, src + size_t(c->q) * blk + off, cnt * sizeof(double2),
+                           cudaMemcpyDeviceToDevice, stream));
   ck(a.GroupStart(), "ncclGroupStart");
   for (int s = 0; s < c->R; ++s) {
     if (s == c->q) continue;
-    ck(a.Send(src + size_t(s) * blk, n, ncclFloat64, s, comm(c), c->stream), "ncclSend");
-    ck(a.Recv(dst + size_t(s) * blk, n, ncclFloat64, s, comm(c), c->stream), "ncclRecv");
+    ck(a.Send(src + size_t(s) * blk + off, n, ncclFloat64, s, comm(c), stream), "ncclSend");
+    ck(a.Recv(dst + size_t(s) * blk + off, n, ncclFloat64, s, comm(c), stream), "ncclRecv");
   }
   ck(a.GroupEnd(), "ncclGroupEnd");
 }

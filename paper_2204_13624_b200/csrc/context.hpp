@@ -205,6 +205,10 @@ struct combo_ctx {
   bool multi = false;     // this context owns peers
   bool in_multi = false;  // rank of a single-process multi-GPU group (outputs are whole-grid arrays)
   bool own_stream = true;
+  // pipelined projection (R > 1): transposes of one Gamma row group run on
+  // comm_stream while the passes of the next group run on stream
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t pipe_ev[12] = {nullptr};
   combo_host::DBuf<double> gpart;              // leader: block partials of all ranks
   combo_host::DBuf<combo_dev::Stats> gstats;   // NCCL: laminate stats of all ranks
   std::unique_ptr<combo_host::FftPlan> plan;
@@ -276,7 +280,8 @@ void nccl_abort(combo_ctx* c);
 void nccl_destroy(combo_ctx* c);
 void nccl_allgather_inplace(combo_ctx* c, double* buf, size_t count_per_rank);
 void nccl_allreduce_u64(combo_ctx* c, const unsigned long long* in, unsigned long long* out, size_t n, bool max);
-void nccl_alltoall_blocks(combo_ctx* c, const double2* src, double2* dst, size_t blk);
+void nccl_alltoall_blocks(combo_ctx* c, const double2* src, double2* dst, size_t blk, size_t off, size_t cnt,
+                          cudaStream_t stream);
 void nccl_allreduce_sum(combo_ctx* c, double* buf, size_t n);
 // engine.cu
 void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths);
@@ -315,7 +320,8 @@ enum ProfTag {
 struct ProfScope {
   combo_ctx* c;
   int idx = -1;
-  ProfScope(combo_ctx* ctx, int tag, double bytes);
+  cudaStream_t st = nullptr;
+  ProfScope(combo_ctx* ctx, int tag, double bytes, cudaStream_t stream = nullptr);
   ~ProfScope();
 };
 // device-side CellMaterials binding of one slab (bind.cu)

@@ -244,7 +244,7 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     return v ? std::atoi(v) : dflt;
   };
   p->xminb = knob("COMBO_XMINB", 2);
-  p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
+  p->fuse_mv = knob("COMBO_FUSE_MV", 1) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -382,16 +382,21 @@ int64_t chunk_blocks(const combo_ctx* c) { return (c->N / (c->dims[1] * c->dims[
 
 // slab <-> pencil transpose of the spectrum (SpecView): block s of rank q's
 // slab side is block q of rank s's pencil side
-void exchange(combo_ctx* c, bool to_pencil) {
+// g >= 0: only the components of Gamma row group g (3 g .. 3 g + 2), on
+// `stream` (default: the compute stream)
+void exchange(combo_ctx* c, bool to_pencil, int g = -1, cudaStream_t stream = nullptr) {
   combo_ctx* L = leader(c);
   if (L->R == 1) return;
+  if (!stream) stream = L->stream;
   const FftPlan& p0 = *L->plan;
-  const size_t blk = size_t(9 * p0.ni * p0.nj * p0.n3p);
-  ProfScope ps(L, kTagExchange, 2.0 * double(L->R - 1) * double(blk) * 16.0 * (L->nccl ? 1.0 : double(L->R)));
+  const size_t cs = size_t(p0.ni * p0.nj * p0.n3p);
+  const size_t blk = 9 * cs;
+  const size_t off = g < 0 ? 0 : size_t(3 * g) * cs, cnt = g < 0 ? blk : 3 * cs;
+  ProfScope ps(L, kTagExchange, 2.0 * double(L->R - 1) * double(cnt) * 16.0 * (L->nccl ? 1.0 : double(L->R)), stream);
   if (L->nccl) {
     double2* src = to_pencil ? L->plan->spec.p : L->plan->specB.p;
     double2* dst = to_pencil ? L->plan->specB.p : L->plan->spec.p;
-    nccl_alltoall_blocks(L, src, dst, blk);
+    nccl_alltoall_blocks(L, src, dst, blk, off, cnt, stream);
     return;
   }
   auto ms = members(L);
@@ -401,7 +406,7 @@ void exchange(combo_ctx* c, bool to_pencil) {
                                      : ms[size_t(s)]->plan->specB.p + size_t(q) * blk;
       double2* dst = to_pencil ? ms[size_t(s)]->plan->specB.p + size_t(q) * blk
                                : ms[size_t(q)]->plan->spec.p + size_t(s) * blk;
-      COMBO_CK(cudaMemcpyAsync(dst, src, blk * sizeof(double2), cudaMemcpyDeviceToDevice, L->stream));
+      COMBO_CK(cudaMemcpyAsync(dst + off, src + off, cnt * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
     }
 }
 
@@ -422,15 +427,16 @@ const char* kTagNames[kNumTags] = {"sweep",  "matvec",    "zfwd",      "yfwd",  
 }  // namespace
 
 // emulated ranks record into the leader's profile (they share its stream)
-ProfScope::ProfScope(combo_ctx* ctx, int tag, double bytes) : c(ctx->lead ? ctx->lead : ctx) {
+ProfScope::ProfScope(combo_ctx* ctx, int tag, double bytes, cudaStream_t stream)
+    : c(ctx->lead ? ctx->lead : ctx), st(stream ? stream : (ctx->lead ? ctx->lead : ctx)->stream) {
   if (!c->prof_on) return;
   combo_ctx::ProfRec r{tag, pool_event(c), pool_event(c), bytes};
-  COMBO_CK(cudaEventRecord(r.a, c->stream));
+  COMBO_CK(cudaEventRecord(r.a, st));
   idx = int(c->prof.size());
   c->prof.push_back(r);
 }
 ProfScope::~ProfScope() {
-  if (idx >= 0) cudaEventRecord(c->prof[size_t(idx)].b, c->stream);
+  if (idx >= 0) cudaEventRecord(c->prof[size_t(idx)].b, st);
 }
 
 double spec_bytes(const combo_ctx* c) {
@@ -529,11 +535,61 @@ void launch_matvec(combo_ctx* c, const MatvecArgs& a, double* q) {
     launch_matvec_bulk<false, false>(c, a, q);
 }
 
+// CG matvec fused with the z-forward pass (k_matvec_zfwd): rows 16-byte
+// aligned, z-lines of 256 or 512 cells (a whole number of matvec tiles whose
+// pair-line buffer leaves room for two ring stages)
+bool mv_zfwd_ok(const combo_ctx* c, const MatvecArgs& a) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const int64_t n3 = c->plan->dims[2];
+  return c->plan->mv_bulk && (n3 == 256 || n3 == 512) && al16(a.r) && al16(a.fin) && al16(a.pdir) &&
+         (a.xv == nullptr || al16(a.xv)) && al16(a.cd.cid);
+}
+
+template <bool FIRST, bool HASX, int L>
+void launch_matvec_zfwd_t(combo_ctx* c, const MatvecArgs& a) {
+  using S = combo_dev::MvStage<FIRST, HASX>;
+  using Z = combo_dev::MvZf<L>;
+  constexpr int kMaxSmem = 227 * 1024;
+  const int stages = std::min(4, (kMaxSmem - Z::kHead - Z::kWork) / S::kBytes);
+  const size_t smem = size_t(Z::kHead + Z::kWork) + size_t(stages) * S::kBytes;
+  auto kern = combo_dev::k_matvec_zfwd<FIRST, HASX, L>;
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    COMBO_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  FftPlan& p = *c->plan;
+  const int64_t nlines = p.ni * p.dims[1];
+  const int grid = int(std::min<int64_t>(nlines, c->num_sms));
+  kern<<<grid, combo_dev::kMvT + 32, smem, c->stream>>>(a, p.sv(), p.ax[2].tw.p, stages);
+}
+
+template <int L>
+void launch_matvec_zfwd(combo_ctx* c, const MatvecArgs& a) {
+  if (a.first)
+    launch_matvec_zfwd_t<true, false, L>(c, a);
+  else if (a.xv)
+    launch_matvec_zfwd_t<false, true, L>(c, a);
+  else
+    launch_matvec_zfwd_t<false, false, L>(c, a);
+}
+
 template <class Prod>
 int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
   FftPlan& p = *c->plan;
   int64_t nb = 0;
   ProfScope ps(c, Prod::CELL ? kTagMvZfwd : kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
+  if constexpr (std::is_same_v<Prod, ProdMatvec>) {
+    if (mv_zfwd_ok(c, prod.a)) {
+      if (p.dims[2] == 512)
+        launch_matvec_zfwd<9>(c, prod.a);
+      else
+        launch_matvec_zfwd<8>(c, prod.a);
+      ++c->launches;
+      COMBO_CK(cudaGetLastError());
+      return p.ni * p.dims[1];
+    }
+  }
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
@@ -583,14 +639,17 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
   return nb;
 }
 
+// components [c0, c0 + ncomp)
 template <bool INV>
-void launch_y(combo_ctx* c, int ncomp = 9) {
+void launch_y(combo_ctx* c, int ncomp = 9, int c0 = 0) {
   FftPlan& p = *c->plan;
   ProfScope ps(c, INV ? kTagYinv : kTagYfwd, 2.0 * spec_bytes(c) * ncomp / 9.0);
+  combo_dev::SpecView svy = p.sv();
+  svy.spec += int64_t(c0) * svy.cs;
   dispatch_log2(p.dims[1], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 6) {
-      if (p.tma_y) {
+      if (p.tma_y && c0 == 0) {
         auto go = [&](auto k, int W) {
           const size_t smem = size_t((p.dims[1] + p.dims[1] / 8) * W) * sizeof(double2);
           dim3 grid(unsigned((p.n3c + W - 1) / W), unsigned(p.ni), unsigned(ncomp));
@@ -609,26 +668,27 @@ void launch_y(combo_ctx* c, int ncomp = 9) {
       dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_rr<L, INV>;
       smem_attr(k, p.rysmem);
-      k<<<grid, p.ryT, p.rysmem, c->stream>>>(p.sv(), p.ax[1].tw.p, p.ryW, ahead_blocks(c, k, p.ryT, p.rysmem));
+      k<<<grid, p.ryT, p.rysmem, c->stream>>>(svy, p.ax[1].tw.p, p.ryW, ahead_blocks(c, k, p.ryT, p.rysmem));
     } else {
       dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_kernel<L, INV>;
       smem_attr(k, p.ysmem);
-      k<<<grid, p.yT, p.ysmem, c->stream>>>(p.sv(), p.ax[1].view(), p.yW);
+      k<<<grid, p.yT, p.ysmem, c->stream>>>(svy, p.ax[1].view(), p.yW);
     }
   });
   ++c->launches;
   COMBO_CK(cudaGetLastError());
 }
 
-void launch_xgamma(combo_ctx* c, int kind) {
+// Gamma row groups [rg0, rg0 + nrg)
+void launch_xgamma(combo_ctx* c, int kind, int rg0 = 0, int nrg = 3) {
   const GreenTables g = green_view(green_plan(c, kind));
   FftPlan& p = *c->plan;
-  ProfScope ps(c, kTagXGamma, 2.0 * spec_bytes(c));
+  ProfScope ps(c, kTagXGamma, 2.0 * spec_bytes(c) * nrg / 3.0);
   dispatch_log2(p.dims[0], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 6) {
-      if (p.tma_x) {
+      if (p.tma_x && rg0 == 0 && nrg == 3) {
         constexpr int W = combo_dev::kTmaW;
         const size_t smem = size_t(3 * p.dims[0] * W) * sizeof(double2);
         dim3 grid(unsigned((p.n3c + W - 1) / W), unsigned(p.nj), 3u);
@@ -647,10 +707,11 @@ void launch_xgamma(combo_ctx* c, int kind) {
     }
     if constexpr (L >= 3) {
       // rank-1 x + Gamma (fft_rr.cuh): two channels per thread
-      dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), 3u);
+      dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), unsigned(nrg));
       auto go = [&](auto k) {
         smem_attr(k, p.rxsmem);
-        k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g, ahead_blocks(c, k, p.rxT, p.rxsmem));
+        k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g, ahead_blocks(c, k, p.rxT, p.rxsmem),
+                                               rg0);
       };
       auto by_kind = [&](auto k0, auto k1, auto k2) {
         if (kind == 0)
@@ -667,10 +728,10 @@ void launch_xgamma(combo_ctx* c, int kind) {
       else
         by_kind(xgamma_v4<L, 0, 256, 2>, xgamma_v4<L, 1, 256, 2>, xgamma_v4<L, 2, 256, 2>);
     } else {
-      dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.nj), 3u);
+      dim3 grid(unsigned((p.n3c + p.xW - 1) / p.xW), unsigned(p.nj), unsigned(nrg));
       auto k = xgamma_kernel<L>;
       smem_attr(k, p.xsmem);
-      k<<<grid, p.xT, p.xsmem, c->stream>>>(p.svB(), p.ax[0].view(), p.xW, g);
+      k<<<grid, p.xT, p.xsmem, c->stream>>>(p.svB(), p.ax[0].view(), p.xW, g, rg0);
     }
   });
   ++c->launches;
@@ -700,6 +761,20 @@ void launch_x_plain(combo_ctx* c) {
   COMBO_CK(cudaGetLastError());
 }
 
+// COMBO_OVERLAP=0: serial transposes (exchange -> x + Gamma -> exchange)
+bool overlap_knob() {
+  static const bool v = [] {
+    const char* s = std::getenv("COMBO_OVERLAP");
+    return s ? std::atoi(s) != 0 : true;
+  }();
+  return v;
+}
+void pipe_init(combo_ctx* c) {
+  if (c->comm_stream) return;
+  COMBO_CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+  for (auto& e : c->pipe_ev) COMBO_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
 // Projection Pi(tau) = alpha Gamma^0 tau (green.cpp:133-151) with fused
 // producer / consumer, over every rank hosted by the leader c: prodf(k) /
 // consf(k) build member k's producer and consumer. z and y passes run on
@@ -713,11 +788,39 @@ void project_group(combo_ctx* c, int kind, PF&& prodf, CF&& consf, int slot_cons
   using Cons = std::decay_t<decltype(consf(size_t(0)))>;
   static_assert(Prod::NRED == 0, "producer reductions are not combined across ranks");
   for (size_t k = 0; k < ms.size(); ++k) launch_zfwd(ms[k], prodf(k), prod_bytes);
-  for (auto* m : ms) launch_y<false>(m);
-  exchange(c, true);
-  for (auto* m : ms) launch_xgamma(m, kind);
-  exchange(c, false);
-  for (auto* m : ms) launch_y<true>(m);
+  if (c->R > 1 && overlap_knob()) {
+    // Gamma couples only the components of one row group (green.cpp:114-127):
+    // the transposes of group g run on the comm stream while the y / x
+    // passes of the neighbouring groups run on the compute stream
+    pipe_init(c);
+    cudaStream_t cs = c->stream, xs = c->comm_stream;
+    cudaEvent_t* ev = c->pipe_ev;  // [g]: y fwd done, [3+g]: to pencils done, [6+g]: x done, [9+g]: back done
+    for (int g = 0; g < 3; ++g) {
+      for (auto* m : ms) launch_y<false>(m, 3, 3 * g);
+      COMBO_CK(cudaEventRecord(ev[g], cs));
+      COMBO_CK(cudaStreamWaitEvent(xs, ev[g], 0));
+      exchange(c, true, g, xs);
+      COMBO_CK(cudaEventRecord(ev[3 + g], xs));
+    }
+    for (int g = 0; g < 3; ++g) {
+      COMBO_CK(cudaStreamWaitEvent(cs, ev[3 + g], 0));
+      for (auto* m : ms) launch_xgamma(m, kind, g, 1);
+      COMBO_CK(cudaEventRecord(ev[6 + g], cs));
+      COMBO_CK(cudaStreamWaitEvent(xs, ev[6 + g], 0));
+      exchange(c, false, g, xs);
+      COMBO_CK(cudaEventRecord(ev[9 + g], xs));
+    }
+    for (int g = 0; g < 3; ++g) {
+      COMBO_CK(cudaStreamWaitEvent(cs, ev[9 + g], 0));
+      for (auto* m : ms) launch_y<true>(m, 3, 3 * g);
+    }
+  } else {
+    for (auto* m : ms) launch_y<false>(m);
+    exchange(c, true);
+    for (auto* m : ms) launch_xgamma(m, kind);
+    exchange(c, false);
+    for (auto* m : ms) launch_y<true>(m);
+  }
   int64_t nbc = 0;
   for (size_t k = 0; k < ms.size(); ++k) nbc = launch_zinv(ms[k], consf(k));
   if (Cons::NRED) group_reduce(c, nbc, Cons::NRED, slot_cons);
@@ -1145,7 +1248,7 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
                            rk_[k].N, P(x_, k), step_prev}};
       };
       const double mvb = (it == 0 ? 220.0 : 436.0) * double(c_->N) + 360.0 * double(c_->ncomp);
-      if (c_->plan->fuse_mv) {
+      if (c_->plan->fuse_mv && mv_zfwd_ok(rk_[0].c, mv(0).a)) {
         project_group(c_, cfg_.green, mv, cons, 20, mvb);
       } else {
         for (size_t k = 0; k < rk_.size(); ++k) {
@@ -1628,6 +1731,11 @@ int combo_ctx_destroy(combo_ctx* c) {
   }
   c->plan.reset();
   if (c->hres) cudaFreeHost(c->hres);
+  if (c->comm_stream) {
+    cudaStreamDestroy(c->comm_stream);
+    for (auto e : c->pipe_ev)
+      if (e) cudaEventDestroy(e);
+  }
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return COMBO_OK;

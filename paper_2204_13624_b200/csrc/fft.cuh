@@ -493,10 +493,11 @@ __device__ __forceinline__ void gamma_row(const GreenTables& G, int row, int64_t
 
 // X pass fused with Gamma: grid (column tiles, n2, 3 row groups)
 template <int LOG2N>
-static __global__ void __launch_bounds__(kMaxFftThreads) xgamma_kernel(SpecView sv, Axis ax, int W, GreenTables G) {
+static __global__ void __launch_bounds__(kMaxFftThreads) xgamma_kernel(SpecView sv, Axis ax, int W, GreenTables G,
+                                                                       int rg0) {
   extern __shared__ double2 sm[];
   const int n1 = line_len<LOG2N>(ax);
-  const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
+  const int rg = rg0 + blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
   const int W3 = 3 * W;
   const int64_t plane = sv.cs;  // component stride

@@ -87,13 +87,26 @@ __device__ __forceinline__ int rr_in(int u, int q, int r) {
   return u + q * (N / 8) + r * (N / R);
 }
 
+// barrier of the threads that exchange through sm: the whole block, or a
+// named barrier over a warp-aligned group of it
+struct BlockSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct GroupSync {
+  int id, count;  // barrier 1..15, threads (a multiple of 32)
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  }
+};
+
 // Stages S.. of the transform on C channels held in v. addr(ch, pos) gives
 // the shared-memory slot of channel ch at line position pos (per thread's
-// line). All threads of the block must call this (barriers inside).
-template <int L, bool INV, bool REV, int S, int C, class Addr>
+// line). All threads of the block (of the sync group) must call this
+// (barriers inside).
+template <int L, bool INV, bool REV, int S, int C, class Addr, class Sync = BlockSync>
 __device__ __forceinline__ void rr_stages_w(double2 (&v)[C][8], int u, bool active, double2* sm,
                                             const double2* __restrict__ tw, const Addr& addr,
-                                            const double2 (&w)[8 / Seq<L, REV>::R(S)]) {
+                                            const double2 (&w)[8 / Seq<L, REV>::R(S)], const Sync& sync = Sync()) {
   using Q = Seq<L, REV>;
   constexpr int N = Q::N, R = Q::R(S), P = Q::P(S);
   if (active) {
@@ -112,7 +125,7 @@ __device__ __forceinline__ void rr_stages_w(double2 (&v)[C][8], int u, bool acti
 #pragma unroll
           for (int r = 0; r < R; ++r) sm[addr(ch, rr_out<N, R, P>(u, q, r))] = v[ch][q * R + r];
     }
-    __syncthreads();
+    sync();
     if (active) {
 #pragma unroll
       for (int ch = 0; ch < C; ++ch)
@@ -121,22 +134,23 @@ __device__ __forceinline__ void rr_stages_w(double2 (&v)[C][8], int u, bool acti
 #pragma unroll
           for (int r = 0; r < R2; ++r) v[ch][q * R2 + r] = sm[addr(ch, rr_in<N, R2>(u, q, r))];
     }
-    __syncthreads();
-    rr_stages_w<L, INV, REV, S + 1, C>(v, u, active, sm, tw, addr, wn);
+    sync();
+    rr_stages_w<L, INV, REV, S + 1, C>(v, u, active, sm, tw, addr, wn, sync);
   }
 }
 
 // Stages S.. of the transform on C channels held in v. addr(ch, pos) gives
 // the shared-memory slot of channel ch at line position pos (per thread's
 // line). All threads of the block must call this (barriers inside).
-template <int L, bool INV, bool REV, int S, int C, class Addr>
+template <int L, bool INV, bool REV, int S, int C, class Addr, class Sync = BlockSync>
 __device__ __forceinline__ void rr_stages(double2 (&v)[C][8], int u, bool active, double2* sm,
-                                          const double2* __restrict__ tw, const Addr& addr) {
+                                          const double2* __restrict__ tw, const Addr& addr,
+                                          const Sync& sync = Sync()) {
   using Q = Seq<L, REV>;
   if constexpr (S < Q::NS) {
     double2 w[8 / Q::R(S)];
     rr_twload<Q::N, Q::R(S), Q::P(S)>(w, u, tw);
-    rr_stages_w<L, INV, REV, S, C>(v, u, active, sm, tw, addr, w);
+    rr_stages_w<L, INV, REV, S, C>(v, u, active, sm, tw, addr, w, sync);
   }
 }
 
@@ -560,16 +574,16 @@ __device__ __forceinline__ void rank_gamma(const GreenTables& G, const RankCol<K
 
 template <int L, int KIND, int MAXT, int MINB>
 static __global__ void __launch_bounds__(MAXT, MINB)
-    xgamma_v4(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G, int ahead) {
+    xgamma_v4(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G, int ahead, int rg0) {
   constexpr int N = 1 << L;
   extern __shared__ double2 sm[];
-  const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
+  const int rg = rg0 + blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
   const int64_t plane = sv.cs;
   prefetch_ahead(ahead, 3 * N, [&](int b0, int b1, int b2, int t) {
-    return sv.spec + int64_t(3 * b2 + t / N) * plane + b0 * W + sv.rowB(t % N, b1);
+    return sv.spec + int64_t(3 * (rg0 + b2) + t / N) * plane + b0 * W + sv.rowB(t % N, b1);
   });
   double2* base = sv.spec + int64_t(3 * rg) * plane + kc0 + line;  // pencil side, local k2 j
   const RankCol<KIND> col = rank_col<KIND>(G, rg, sv.j0 + j, kc0 + line, sv.n2, sv.n3);
