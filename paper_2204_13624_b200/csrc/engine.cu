@@ -244,7 +244,8 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     return v ? std::atoi(v) : dflt;
   };
   p->xminb = knob("COMBO_XMINB", 2);
-  p->fuse_mv = knob("COMBO_FUSE_MV", 1) != 0;
+  p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
+  p->zbulk = knob("COMBO_ZBULK", 1) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -535,61 +536,11 @@ void launch_matvec(combo_ctx* c, const MatvecArgs& a, double* q) {
     launch_matvec_bulk<false, false>(c, a, q);
 }
 
-// CG matvec fused with the z-forward pass (k_matvec_zfwd): rows 16-byte
-// aligned, z-lines of 256 or 512 cells (a whole number of matvec tiles whose
-// pair-line buffer leaves room for two ring stages)
-bool mv_zfwd_ok(const combo_ctx* c, const MatvecArgs& a) {
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  const int64_t n3 = c->plan->dims[2];
-  return c->plan->mv_bulk && (n3 == 256 || n3 == 512) && al16(a.r) && al16(a.fin) && al16(a.pdir) &&
-         (a.xv == nullptr || al16(a.xv)) && al16(a.cd.cid);
-}
-
-template <bool FIRST, bool HASX, int L>
-void launch_matvec_zfwd_t(combo_ctx* c, const MatvecArgs& a) {
-  using S = combo_dev::MvStage<FIRST, HASX>;
-  using Z = combo_dev::MvZf<L>;
-  constexpr int kMaxSmem = 227 * 1024;
-  const int stages = std::min(4, (kMaxSmem - Z::kHead - Z::kWork) / S::kBytes);
-  const size_t smem = size_t(Z::kHead + Z::kWork) + size_t(stages) * S::kBytes;
-  auto kern = combo_dev::k_matvec_zfwd<FIRST, HASX, L>;
-  static bool attr = false;  // per instantiation
-  if (!attr) {
-    COMBO_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
-  FftPlan& p = *c->plan;
-  const int64_t nlines = p.ni * p.dims[1];
-  const int grid = int(std::min<int64_t>(nlines, c->num_sms));
-  kern<<<grid, combo_dev::kMvT + 32, smem, c->stream>>>(a, p.sv(), p.ax[2].tw.p, stages);
-}
-
-template <int L>
-void launch_matvec_zfwd(combo_ctx* c, const MatvecArgs& a) {
-  if (a.first)
-    launch_matvec_zfwd_t<true, false, L>(c, a);
-  else if (a.xv)
-    launch_matvec_zfwd_t<false, true, L>(c, a);
-  else
-    launch_matvec_zfwd_t<false, false, L>(c, a);
-}
-
 template <class Prod>
 int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
   FftPlan& p = *c->plan;
   int64_t nb = 0;
   ProfScope ps(c, Prod::CELL ? kTagMvZfwd : kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
-  if constexpr (std::is_same_v<Prod, ProdMatvec>) {
-    if (mv_zfwd_ok(c, prod.a)) {
-      if (p.dims[2] == 512)
-        launch_matvec_zfwd<9>(c, prod.a);
-      else
-        launch_matvec_zfwd<8>(c, prod.a);
-      ++c->launches;
-      COMBO_CK(cudaGetLastError());
-      return p.ni * p.dims[1];
-    }
-  }
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
@@ -623,9 +574,18 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
     if constexpr (L >= 3) {
       nb = (p.ni * p.dims[1] + p.rzL - 1) / p.rzL;
       double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
-      auto k = zinv_rr<Cons, L>;
-      smem_attr(k, p.rzsmem);
-      k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
+      const size_t rows = size_t(9 * p.rzL) * size_t(p.n3p) * sizeof(double2);
+      if (p.zbulk && p.rzsmem % 128 == 0 && p.rzsmem + rows <= 100 * 1024) {
+        // spectrum rows staged by cp.async.bulk behind the pair lines
+        auto k = zinv_bulk<Cons, L>;
+        smem_attr(k, p.rzsmem + rows);
+        k<<<unsigned(nb), p.rzT, p.rzsmem + rows, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL,
+                                                              int(p.rzsmem / sizeof(double2)), scale, cons, part);
+      } else {
+        auto k = zinv_rr<Cons, L>;
+        smem_attr(k, p.rzsmem);
+        k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
+      }
     } else {
       nb = (p.ni * p.dims[1] + p.zL - 1) / p.zL;
       double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
@@ -1248,7 +1208,7 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
                            rk_[k].N, P(x_, k), step_prev}};
       };
       const double mvb = (it == 0 ? 220.0 : 436.0) * double(c_->N) + 360.0 * double(c_->ncomp);
-      if (c_->plan->fuse_mv && mv_zfwd_ok(rk_[0].c, mv(0).a)) {
+      if (c_->plan->fuse_mv) {
         project_group(c_, cfg_.green, mv, cons, 20, mvb);
       } else {
         for (size_t k = 0; k < rk_.size(); ++k) {

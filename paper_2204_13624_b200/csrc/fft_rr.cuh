@@ -13,6 +13,7 @@
 #pragma once
 
 #include "fft.cuh"
+#include "stage.cuh"
 
 namespace combo_dev {
 
@@ -198,9 +199,10 @@ __device__ __forceinline__ void prefetch_ahead(int ahead, int nrows, const Rows&
 // (component a, component b) pair; per group: NSC scalars, plus per-component
 // sums of a and b when PERCOMP. Deterministic fixed-order combination into
 // partials[block][NSC + (PERCOMP ? 9 : 0)].
-template <int NSC, bool PERCOMP>
+template <int NSC, bool PERCOMP, class Sync = BlockSync>
 __device__ void group_reduce_store(double (&sc)[NSC > 0 ? NSC : 1], double pa, double pb, int ca, int cb, int G,
-                                   double* red_sm, double* partials, int64_t block) {
+                                   double* red_sm, double* partials, int64_t block, int tid = threadIdx.x,
+                                   int nthreads = blockDim.x, const Sync& sync = Sync()) {
   constexpr int NV = NSC + (PERCOMP ? 2 : 0);
   if constexpr (NV > 0) {
     double v[NV > 0 ? NV : 1];
@@ -210,13 +212,13 @@ __device__ void group_reduce_store(double (&sc)[NSC > 0 ? NSC : 1], double pa, d
       v[NSC] = pa;
       v[NSC + 1] = pb;
     }
-    const int lane = threadIdx.x & 31;
+    const int lane = tid & 31;
     const int g = G < 32 ? G : 32;
 #pragma unroll
     for (int i = 0; i < NV; ++i)
       for (int o = g >> 1; o > 0; o >>= 1) v[i] += __shfl_down_sync(0xffffffffu, v[i], o, g);
-    const int ngroups = (blockDim.x + g - 1) / g;
-    const int grp = threadIdx.x / g;
+    const int ngroups = (nthreads + g - 1) / g;
+    const int grp = tid / g;
     // red_sm: [ngroups][NV + 2] (values, ca, cb)
     if ((lane & (g - 1)) == 0) {
 #pragma unroll
@@ -224,11 +226,11 @@ __device__ void group_reduce_store(double (&sc)[NSC > 0 ? NSC : 1], double pa, d
       red_sm[grp * (NV + 2) + NV] = double(ca);
       red_sm[grp * (NV + 2) + NV + 1] = double(cb);
     }
-    __syncthreads();
+    sync();
     constexpr int NOUT = NSC + (PERCOMP ? 9 : 0);
-    if (int(threadIdx.x) < NOUT) {
+    if (tid < NOUT) {
       double s = 0.0;
-      const int o = threadIdx.x;
+      const int o = tid;
       for (int gi = 0; gi < ngroups; ++gi) {
         const double* e = red_sm + gi * (NV + 2);
         if (o < NSC) {
@@ -328,6 +330,47 @@ static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
   zfwd_tile<Prod, L>(sv, tw, line0, int(min(int64_t(nl_per_block), nlines_tot - line0)), prod);
 }
 
+// Second half of a z-inverse tile: the completed natural-order pair lines
+// are in sm; inverse stages, then the consumer on the real outputs.
+template <class Cons, int L, class Sync = BlockSync>
+__device__ __forceinline__ void zinv_finish(double2* sm, const double2* __restrict__ tw, int64_t line0, int nreal,
+                                            int npair, double scale, const Cons& cons, double* partials,
+                                            int64_t slot, int tid = threadIdx.x, int nthreads = blockDim.x,
+                                            const Sync& sync = Sync()) {
+  constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
+  const int u = tid % TL, p = tid / TL;
+  const bool active = p < npair;
+  double2 v[1][8];
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[0][i] = sm[p * LS + pad8(rr_first_pos<L, false>(u, i))];
+  }
+  sync();
+  auto addr = [&](int, int pos) { return p * LS + pad8(pos); };
+  rr_stages<L, true, false, 0, 1>(v, u, active, sm, tw, addr, sync);
+  const int rla = 2 * p, rlb = 2 * p + 1;
+  const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
+  const bool hasb = rlb < nreal;
+  double sc[Cons::NSC > 0 ? Cons::NSC : 1];
+#pragma unroll
+  for (int i = 0; i < (Cons::NSC > 0 ? Cons::NSC : 1); ++i) sc[i] = 0.0;
+  double pa = 0.0, pb = 0.0;
+  if (active) {
+    const int64_t cella = (line0 + la) * N, cellb = (line0 + lb) * N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = rr_final_pos<L, false>(u, i);
+      pa += cons.comp(ca, cella + e, v[0][i].x * scale, sc);
+      if (hasb) pb += cons.comp(cb, cellb + e, v[0][i].y * scale, sc);
+    }
+  }
+  if constexpr (Cons::NSC > 0 || Cons::PERCOMP) {
+    sync();  // sm reused for the group reduction
+    group_reduce_store<Cons::NSC, Cons::PERCOMP>(sc, pa, pb, ca, active && hasb ? cb : -1, TL,
+                                                 reinterpret_cast<double*>(sm), partials, slot, tid, nthreads, sync);
+  }
+}
+
 // one tile: z-lines [line0, line0 + nlines); partial sums -> partials[slot].
 // CG: spectrum loads bypass L1 (the fused Y/Z kernel reads rows other SMs
 // just wrote); DISCARD: the consumed spectrum rows are dropped from L2
@@ -336,7 +379,7 @@ template <class Cons, int L, bool CG = false, bool DISCARD = false>
 __device__ __forceinline__ void zinv_tile(const SpecView& sv, const double2* __restrict__ tw, int64_t line0,
                                           int nlines, double scale, const Cons& cons, double* partials,
                                           int64_t slot, bool discard = true) {
-  constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
+  constexpr int N = 1 << L, LS = N + N / 8;
   extern __shared__ double2 sm[];
   const int nreal = 9 * nlines;
   const int npair = (nreal + 1) >> 1;
@@ -397,37 +440,7 @@ __device__ __forceinline__ void zinv_tile(const SpecView& sv, const double2* __r
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
     }
   }
-  const int u = threadIdx.x % TL, p = threadIdx.x / TL;
-  const bool active = p < npair;
-  double2 v[1][8];
-  if (active) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[0][i] = sm[p * LS + pad8(rr_first_pos<L, false>(u, i))];
-  }
-  __syncthreads();
-  auto addr = [&](int, int pos) { return p * LS + pad8(pos); };
-  rr_stages<L, true, false, 0, 1>(v, u, active, sm, tw, addr);
-  const int rla = 2 * p, rlb = 2 * p + 1;
-  const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
-  const bool hasb = rlb < nreal;
-  double sc[Cons::NSC > 0 ? Cons::NSC : 1];
-#pragma unroll
-  for (int i = 0; i < (Cons::NSC > 0 ? Cons::NSC : 1); ++i) sc[i] = 0.0;
-  double pa = 0.0, pb = 0.0;
-  if (active) {
-    const int64_t cella = (line0 + la) * N, cellb = (line0 + lb) * N;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = rr_final_pos<L, false>(u, i);
-      pa += cons.comp(ca, cella + e, v[0][i].x * scale, sc);
-      if (hasb) pb += cons.comp(cb, cellb + e, v[0][i].y * scale, sc);
-    }
-  }
-  if constexpr (Cons::NSC > 0 || Cons::PERCOMP) {
-    __syncthreads();  // sm reused for the group reduction
-    group_reduce_store<Cons::NSC, Cons::PERCOMP>(sc, pa, pb, ca, active && hasb ? cb : -1, TL,
-                                                 reinterpret_cast<double*>(sm), partials, slot);
-  }
+  zinv_finish<Cons, L>(sm, tw, line0, nreal, npair, scale, cons, partials, slot);
 }
 
 template <class Cons, int L>
@@ -438,6 +451,143 @@ static __global__ void __launch_bounds__(512, 2)
   const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
   zinv_tile<Cons, L>(sv, tw, line0, int(min(int64_t(nl_per_block), nlines_tot - line0)), scale, cons, partials,
                      blockIdx.x);
+}
+
+// Bulk-staged z-inverse: one thread fetches the tile's spectrum rows (n3c
+// complex each, contiguous) with cp.async.bulk into shared memory behind the
+// pair lines; the Hermitian completion then reads shared memory, so no warp
+// waits on HBM loads in registers. rows_off = offset of the row buffer in sm.
+template <class Cons, int L>
+static __global__ void __launch_bounds__(512, 2)
+    zinv_bulk(SpecView sv, const double2* __restrict__ tw, int nl_per_block, int rows_off, double scale, Cons cons,
+              double* partials) {
+  constexpr int N = 1 << L, LS = N + N / 8;
+  extern __shared__ __align__(128) double2 sm[];
+  __shared__ uint64_t bar;
+  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
+  const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
+  const int nlines = int(min(int64_t(nl_per_block), nlines_tot - line0));
+  const int nreal = 9 * nlines;
+  const int npair = (nreal + 1) >> 1;
+  const int nc = int(sv.n3c);
+  const int ncr = (nc + 31) & ~31;  // warp-aligned k ranges (see zfwd_rr)
+  double2* rows = sm + rows_off;
+  const int n3p = int(sv.n3p);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    const uint32_t rb = uint32_t(nc) * 16u;
+    mbar_expect_tx(&bar, rb * uint32_t(nreal));
+    for (int rl = 0; rl < nreal; ++rl)
+      bulk_g2s(rows + rl * n3p, sv.spec + sv.zrow(rl % 9, line0 + rl / 9), rb, &bar);
+  }
+  if (threadIdx.x >= 32 && threadIdx.x < 41) cons.prefetch(int(threadIdx.x) - 32, line0 * N, int64_t(nlines) * N);
+  __syncthreads();  // barrier initialised before anyone polls it
+  mbar_wait(&bar, 0);
+  // Hermitian completion of the pair (halfcomplex c2r: DC/Nyquist imaginary
+  // parts ignored) into natural-order smem lines
+  for (int t = threadIdx.x; t < npair * ncr; t += blockDim.x) {
+    const int pp = t / ncr, k = t - pp * ncr;
+    if (k >= nc) continue;
+    const int rl = 2 * pp;
+    double2 xa = rows[rl * n3p + k];
+    double2 xb = rl + 1 < nreal ? rows[(rl + 1) * n3p + k] : make_double2(0.0, 0.0);
+    const bool selfconj = (k == 0) || (2 * k == N);
+    if (selfconj) {
+      xa.y = 0.0;
+      xb.y = 0.0;
+    }
+    sm[pp * LS + pad8(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+    if (!selfconj) sm[pp * LS + pad8(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+  }
+  __syncthreads();
+  zinv_finish<Cons, L>(sm, tw, line0, nreal, npair, scale, cons, partials, blockIdx.x);
+}
+
+// Persistent ring-staged z-inverse for z-lines of 256 / 512 cells (one line
+// per tile): one block per SM; a producer lane streams the 9 spectrum rows
+// of each tile into a ring of shared-memory stages with cp.async.bulk (and
+// L2-prefetches the consumer's field rows); two consumer groups of
+// 5 N/8 threads take alternate tiles -- Hermitian completion from the stage
+// into the group's pair lines, inverse stages with a named barrier over the
+// group, consumer epilogue -- so the completion / transform / epilogue phases
+// of one tile overlap the other group's and the loads of the next tiles.
+// Partials are indexed by tile: same values and order as zinv_rr.
+template <int L>
+struct ZRing {
+  static constexpr int N = 1 << L, LS = N + N / 8, NP = 5, GT = NP * (N / 8);  // threads per consumer group
+  static constexpr int kHead = 128;
+  static constexpr int kWork = NP * LS * 16;  // pair lines of one group
+  static constexpr int kThreads = 2 * GT + 32;
+};
+
+template <class Cons, int L>
+static __global__ void __launch_bounds__(ZRing<L>::kThreads, 1)
+    zinv_ring(SpecView sv, const double2* __restrict__ tw, double scale, Cons cons, double* partials, int nstages) {
+  using Z = ZRing<L>;
+  constexpr int N = Z::N, LS = Z::LS, NP = Z::NP, GT = Z::GT;
+  extern __shared__ __align__(128) unsigned char zr_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(zr_raw);
+  uint64_t* empty = full + 8;
+  const int n3p = int(sv.n3p), nc = int(sv.n3c);
+  const int ncr = (nc + 31) & ~31;  // warp-aligned k ranges (see zfwd_rr)
+  const uint32_t stage_bytes = uint32_t(9 * n3p) * 16u;
+  unsigned char* stages = zr_raw + Z::kHead + 2 * Z::kWork;
+  const int64_t ntiles = sv.ni * sv.n2;  // local z-lines
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], GT / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (int(threadIdx.x) >= 2 * GT) {  // producer warp
+    if ((threadIdx.x & 31) == 0) {
+      Ring rg(nstages);
+      int k = 0;
+      const uint32_t rb = uint32_t(nc) * 16u;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k, rg.next()) {
+        if (k >= nstages) mbar_wait(&empty[rg.s], rg.phase ^ 1u);
+        double2* rows = reinterpret_cast<double2*>(stages + size_t(rg.s) * stage_bytes);
+        mbar_expect_tx(&full[rg.s], 9u * rb);
+#pragma unroll 1
+        for (int rl = 0; rl < 9; ++rl) bulk_g2s(rows + rl * n3p, sv.spec + sv.zrow(rl, tile), rb, &full[rg.s]);
+#pragma unroll 1
+        for (int c = 0; c < 9; ++c) cons.prefetch(c, tile * N, N);
+      }
+    }
+    return;
+  }
+  const int g = int(threadIdx.x) / GT, tid = int(threadIdx.x) - g * GT;
+  const GroupSync gsync{1 + g, GT};
+  double2* work = reinterpret_cast<double2*>(zr_raw + Z::kHead + g * Z::kWork);
+  Ring rg(nstages);
+  int k = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k, rg.next()) {
+    if ((k & 1) != g) continue;
+    gsync();  // the previous tile's reduction has left the pair lines
+    mbar_wait(&full[rg.s], rg.phase);
+    const double2* rows = reinterpret_cast<const double2*>(stages + size_t(rg.s) * stage_bytes);
+    // Hermitian completion of the pairs (see zinv_tile) from the staged rows
+    for (int t = tid; t < NP * ncr; t += GT) {
+      const int pp = t / ncr, kk = t - pp * ncr;
+      if (kk >= nc) continue;
+      const int rl = 2 * pp;
+      double2 xa = rows[rl * n3p + kk];
+      double2 xb = rl + 1 < 9 ? rows[(rl + 1) * n3p + kk] : make_double2(0.0, 0.0);
+      const bool selfconj = (kk == 0) || (2 * kk == N);
+      if (selfconj) {
+        xa.y = 0.0;
+        xb.y = 0.0;
+      }
+      work[pp * LS + pad8(kk)] = make_double2(xa.x - xb.y, xa.y + xb.x);
+      if (!selfconj) work[pp * LS + pad8(N - kk)] = make_double2(xa.x + xb.y, xb.x - xa.y);
+    }
+    gsync();  // stage consumed, pair lines complete
+    if ((tid & 31) == 0) mbar_arrive(&empty[rg.s]);
+    zinv_finish<Cons, L>(work, tw, tile, 9, NP, scale, cons, partials, tile, tid, GT, gsync);
+  }
 }
 
 // ------------------------------------------------------------------ Y pass

@@ -517,155 +517,6 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
   }
 }
 
-// Bulk-staged matvec fused with the z-axis r2c of the projection that
-// follows it (solver.cpp:194-197 + Fft3::forward axis 2): the tiles of one
-// z-line (n3 / kMvT ring stages) are evaluated as in k_matvec_bulk, but
-// q = A : pdir goes to a shared-memory line buffer instead of HBM; when the
-// line is complete the consumer warps transform its 9 components (pairs of
-// real lines packed as complex lines, the register-resident stages of
-// zfwd_rr with a named barrier over the consumer threads) and store the 9
-// half-spectrum rows. Saves the q round trip (144 B per boxel and CG
-// iteration). Same arithmetic as k_matvec_bulk + zfwd_rr (bitwise).
-template <int L>
-struct MvZf {
-  static constexpr int N3 = 1 << L, TL = N3 / 8, LS = N3 + N3 / 8, SPL = N3 / kMvT, PPR = kMvT / TL, NP = 5;
-  static constexpr int kHead = 256;                        // barriers (128 B) + spectrum row offsets
-  static constexpr int kWork = NP * LS * 16;               // pair lines
-  static_assert(N3 % kMvT == 0 && kMvT % TL == 0, "z-line must be a whole number of matvec tiles");
-};
-
-template <bool FIRST, bool HASX, int L>
-static __global__ void __launch_bounds__(kMvT + 32, 1)
-    k_matvec_zfwd(MatvecArgs a, SpecView sv, const double2* __restrict__ tw, int nstages) {
-  using S = MvStage<FIRST, HASX>;
-  using Z = MvZf<L>;
-  constexpr int N3 = Z::N3, TL = Z::TL, LS = Z::LS, SPL = Z::SPL, PPR = Z::PPR, NP = Z::NP;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* empty = full + 8;
-  int64_t* zr = reinterpret_cast<int64_t*>(smem_raw + 128);
-  double2* work = reinterpret_cast<double2*>(smem_raw + Z::kHead);
-  unsigned char* buf = smem_raw + Z::kHead + Z::kWork;
-  const int64_t N = a.N;
-  const int64_t nlines = sv.ni * sv.n2;  // local z-lines
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < nstages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kMvT / 32);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (warp == kMvT / 32) {  // producer
-    if (lane == 0) {
-      Ring rg(nstages);
-      int k = 0;
-      for (int64_t line = blockIdx.x; line < nlines; line += gridDim.x) {
-#pragma unroll 1
-        for (int sub = 0; sub < SPL; ++sub, ++k, rg.next()) {
-          if (k >= nstages) mbar_wait(&empty[rg.s], rg.phase ^ 1u);
-          double* d = reinterpret_cast<double*>(buf + size_t(rg.s) * S::kBytes);
-          const int64_t off = line * N3 + sub * kMvT;
-          constexpr uint32_t rb = kMvT * 8;
-          mbar_expect_tx(&full[rg.s], S::kBytes);
-#pragma unroll 1
-          for (int c = 0; c < 9; ++c) {
-            bulk_g2s(d + c * kMvT, a.r + c * N + off, rb, &full[rg.s]);
-            bulk_g2s(d + (9 + c) * kMvT, a.fin + c * N + off, rb, &full[rg.s]);
-            if (!FIRST) bulk_g2s(d + (18 + c) * kMvT, a.pdir + c * N + off, rb, &full[rg.s]);
-            if (!FIRST && HASX) bulk_g2s(d + (27 + c) * kMvT, a.xv + c * N + off, rb, &full[rg.s]);
-          }
-          bulk_g2s(d + S::kRows * kMvT, a.cd.cid + off, kMvT * 4, &full[rg.s]);
-        }
-      }
-    }
-    return;
-  }
-  const int tid = threadIdx.x;
-  const GroupSync csync{1, kMvT};
-  double* smd = reinterpret_cast<double*>(work);
-  const int nc = int(sv.n3c);
-  const int ncr = (nc + 31) & ~31;  // warp-aligned k ranges (see zfwd_rr)
-  Ring rg(nstages);
-  for (int64_t line = blockIdx.x; line < nlines; line += gridDim.x) {
-    if (tid < 9) zr[tid] = sv.zrow(tid, line);
-#pragma unroll 1
-    for (int sub = 0; sub < SPL; ++sub, rg.next()) {
-      mbar_wait(&full[rg.s], rg.phase);
-      const double* d = reinterpret_cast<const double*>(buf + size_t(rg.s) * S::kBytes);
-      const int64_t cell = line * N3 + sub * kMvT + tid;
-      double x[9];
-#pragma unroll
-      for (int c = 0; c < 9; ++c) x[c] = d[c * kMvT + tid];
-      if (!FIRST) {
-#pragma unroll
-        for (int c = 0; c < 9; ++c) {
-          const double po = d[(18 + c) * kMvT + tid];
-          if (HASX) a.xv[c * N + cell] = d[(27 + c) * kMvT + tid] + a.step_prev * po;
-          x[c] += a.beta * po;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 9; ++c) a.pdir[c * N + cell] = x[c];
-      const int32_t id = reinterpret_cast<const int32_t*>(d + S::kRows * kMvT)[tid];
-      double y[9];
-      if (id >= 0) {
-        packed45_apply(a.cd.t45 + id, a.cd.ncomp, x, y);
-      } else {
-        double f[9];
-#pragma unroll
-        for (int c = 0; c < 9; ++c) f[c] = d[(9 + c) * kMvT + tid] + a.sh.v[c];
-        const LawP Lw = id == -2 ? a.M.law[1] : a.M.law[0];
-        NhState s;
-        if (law_state(Lw, f, s))
-          law_apply(Lw, s, x, y);
-        else
-#pragma unroll
-          for (int c = 0; c < 9; ++c) y[c] = x[c];
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[rg.s]);
-      // q of this cell -> pair lines (component c is real line c of the z-line)
-      const int k = sub * kMvT + tid;
-#pragma unroll
-      for (int c = 0; c < 9; ++c) smd[2 * ((c >> 1) * LS + pad8(k)) + (c & 1)] = y[c];
-      smd[2 * ((NP - 1) * LS + pad8(k)) + 1] = 0.0;
-    }
-    csync();
-    // z-axis r2c of the 5 pair lines, PPR lines per round
-#pragma unroll 1
-    for (int rd = 0; rd < (NP + PPR - 1) / PPR; ++rd) {
-      const int p = rd * PPR + tid / TL, u = tid % TL;
-      const bool active = p < NP;
-      double2 v[1][8];
-      if (active) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[0][i] = work[p * LS + pad8(rr_first_pos<L, false>(u, i))];
-      }
-      csync();
-      auto addr = [&](int, int pos) { return p * LS + pad8(pos); };
-      rr_stages<L, false, false, 0, 1>(v, u, active, work, tw, addr, csync);
-      if (active) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) work[p * LS + pad8(rr_final_pos<L, false>(u, i))] = v[0][i];
-      }
-    }
-    csync();
-    // split the pairs into half spectra (zfwd_tile)
-    for (int t = tid; t < NP * ncr; t += kMvT) {
-      const int pp = t / ncr, k = t - pp * ncr;
-      if (k >= nc) continue;
-      const double2 zk = work[pp * LS + pad8(k)];
-      const double2 zm = work[pp * LS + pad8(k == 0 ? 0 : N3 - k)];
-      const int rl = 2 * pp;
-      sv.spec[zr[rl] + k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-      if (rl + 1 < 9) sv.spec[zr[rl + 1] + k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-    }
-    csync();  // line buffer and row offsets are free again
-  }
-}
-
 // Packed effective tangents of all composite cells at (F, warm starts): the
 // tangent half of stress_sweep(tangents45) (cell_material.cpp:146-160),
 // evaluated once per Newton iteration.
