@@ -112,7 +112,8 @@ struct FftPlan {
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
   // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
   // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off
-  bool zbulk = true;  // z-inverse with bulk-staged spectrum rows (COMBO_ZBULK=0: register loads)
+  bool zbulk = false;  // z-inverse with spectrum rows staged per block (COMBO_ZBULK=1; measured slower: 2 blocks/SM)
+  bool zring = true;  // persistent ring-staged z-inverse at n3 = 512 (COMBO_ZRING=0: one block per tile)
   bool tma_x = false, tma_y = false;
   int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
   CUtensorMap xmap{}, ymap{};

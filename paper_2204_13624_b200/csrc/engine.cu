@@ -245,7 +245,8 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   };
   p->xminb = knob("COMBO_XMINB", 2);
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
-  p->zbulk = knob("COMBO_ZBULK", 1) != 0;
+  p->zbulk = knob("COMBO_ZBULK", 0) != 0;
+  p->zring = knob("COMBO_ZRING", 1) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -575,7 +576,22 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
       nb = (p.ni * p.dims[1] + p.rzL - 1) / p.rzL;
       double* part = Cons::NRED ? part_ptr(c, nb, Cons::NRED) : nullptr;
       const size_t rows = size_t(9 * p.rzL) * size_t(p.n3p) * sizeof(double2);
-      if (p.zbulk && p.rzsmem % 128 == 0 && p.rzsmem + rows <= 100 * 1024) {
+      bool ring = false;
+      if constexpr (L == 9) {
+        // persistent ring-staged kernel: one z-line per tile, two consumer groups
+        using Z = combo_dev::ZRing<L>;
+        const int stages = int(std::min<size_t>(4, (227 * 1024 - Z::kHead - 2 * Z::kWork) / rows));
+        if (p.zring && p.rzL == 1 && stages >= 2) {
+          const size_t smem = size_t(Z::kHead + 2 * Z::kWork) + size_t(stages) * rows;
+          auto k = zinv_ring<Cons, L>;
+          smem_attr(k, smem);
+          const int grid = int(std::min<int64_t>(nb, c->num_sms));
+          k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, scale, cons, part, stages);
+          ring = true;
+        }
+      }
+      if (ring) {
+      } else if (p.zbulk && p.rzsmem % 128 == 0 && p.rzsmem + rows <= 100 * 1024) {
         // spectrum rows staged by cp.async.bulk behind the pair lines
         auto k = zinv_bulk<Cons, L>;
         smem_attr(k, p.rzsmem + rows);

@@ -69,16 +69,57 @@ def test_tma_fft_forward_vs_numpy(ctx):
 
 
 @pytest.mark.parametrize("dims", [(16, 8, 512), (8, 8, 64), (4, 12, 256)])
-def test_zinv_bulk_bitwise_equal_register_loads(dims):
-    """zinv_bulk (spectrum rows staged by cp.async.bulk) against zinv_rr."""
+def test_zinv_staged_variants_bitwise_equal_register_loads(dims):
+    """zinv_ring (persistent, spectrum rows through a cp.async.bulk ring, two
+    consumer groups; n3 = 512) and zinv_bulk (rows staged per block) against
+    zinv_rr."""
     rng = np.random.default_rng(21)
     tau = rng.uniform(-1, 1, 9 * int(np.prod(dims)))
     outs = []
-    for z in (1, 0):
-        c, old = _fresh_ctx(COMBO_ZBULK=z)
+    for knobs in (dict(COMBO_ZRING=1), dict(COMBO_ZRING=0, COMBO_ZBULK=0), dict(COMBO_ZRING=0, COMBO_ZBULK=1)):
+        c, old = _fresh_ctx(**knobs)
         try:
             outs.append(c.project(tau, "rotated", dims, (1, 1, 1)))
         finally:
             _restore(old)
             c.close()
-    assert np.array_equal(outs[0].view(np.uint64), outs[1].view(np.uint64))
+    for o in outs[1:]:
+        assert np.array_equal(outs[0].view(np.uint64), o.view(np.uint64))
+
+
+@pytest.mark.parametrize("scheme,green", [("newton_cg", "rotated"), ("basic", "continuous")])
+def test_zinv_ring_solve_bitwise(oracle, scheme, green):
+    """every fused z-inverse consumer (basic update, Newton residual, CG,
+    trial) through the ring kernel: reports and F bitwise equal to the
+    one-block-per-tile kernel, P-bar within 1e-9 of the oracle."""
+    import paper_2204_13624_b200 as pkg
+
+    fine, fac = (16, 24, 1024), (4, 4, 2)
+    dims = tuple(f // k for f, k in zip(fine, fac))
+    fbar = np.eye(3)
+    fbar[0, 0] += 0.04
+    fbar[0, 1] += 0.02
+    runs = []
+    for ring in (1, 0):
+        c, old = _fresh_ctx(COMBO_ZRING=ring)
+        try:
+            img = c.generate("rsa_spheres", fine, (1, 1, 1), 3, 3.0, 6.0, 0.3)
+            kind, cp, _ = c.coarsen(img, fac)
+            nrm, _, _ = c.compute_normals(img, fac, kind)
+            cm = pkg.CellMaterials(c, dims, kind, cp, nrm, pkg.neo_hookean(2.0, 1.0), pkg.neo_hookean(20.0, 10.0))
+            runs.append((cm.solve(fbar, scheme=scheme, green=green, tol_equilibrium=1e-7, load_steps=2,
+                                  max_outer=2000), (kind, cp, nrm)))
+        finally:
+            _restore(old)
+            c.close()
+    (a, grid), (b, _) = runs
+    assert a["report"]["success"] and b["report"]["success"]
+    for sa, sb in zip(a["report"]["steps"], b["report"]["steps"]):
+        assert sa["cg_iters"] == sb["cg_iters"] and sa["residuals"] == sb["residuals"]
+        assert sa["pbar_history"] == sb["pbar_history"]
+    assert np.array_equal(a["f"].view(np.uint64), b["f"].view(np.uint64))
+    kind, cp, nrm = grid
+    cmo = oracle.CellMaterials(dims, kind, cp, nrm, oracle.neo_hookean(2.0, 1.0), oracle.neo_hookean(20.0, 10.0))
+    ro = cmo.solve(fbar, scheme=1 if scheme == "newton_cg" else 0, green={"rotated": 1, "continuous": 0}[green],
+                   tol=1e-7, load_steps=2, max_outer=2000)
+    assert np.linalg.norm(a["pbar"] - ro["pbar"]) <= 1e-9 * np.linalg.norm(ro["pbar"])

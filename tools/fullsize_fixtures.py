@@ -64,8 +64,10 @@ def mem_guard(min_avail_gb=10.0):
     threading.Thread(target=watch, daemon=True).start()
 
 
-def run_case(name, out_dir):
-    case = CASES[name]
+def run_case(name, out_dir, max_ls=None):
+    case = dict(CASES[name])
+    if max_ls is not None:
+        case["max_ls"] = max_ls
     cfg = CONFIGS[case["config"]]
     t0 = time.perf_counter()
     img = O.generate(cfg.shape, cfg.fine, (1.0, 1.0, 1.0), *cfg.params)
@@ -114,11 +116,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("cases", nargs="*", default=list(CASES))
     ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden"))
+    ap.add_argument("--max-ls", type=int, default=None, help="LS budget (default: tests/fullsize_common.py)")
     a = ap.parse_args()
     os.environ.setdefault("OMP_PROC_BIND", "close")
     mem_guard()
     for name in a.cases:
-        run_case(name, a.out)
+        run_case(name, a.out, a.max_ls)
 
 
 if __name__ == "__main__":

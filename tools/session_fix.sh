@@ -6,7 +6,7 @@ mkdir -p gpurun_out/golden
 make -s -C oracle
 ( export OMP_NUM_THREADS=14 OMP_PROC_BIND=close ORACLE_LEAN_TANGENTS=1
   for c in $case; do
-    taskset -c 0-13 timeout $budget python tools/fullsize_fixtures.py $c --out gpurun_out/golden > gpurun_out/golden/log_$c.txt 2>&1
+    taskset -c 0-13 timeout $budget python tools/fullsize_fixtures.py $c --out gpurun_out/golden $FIXTURE_ARGS > gpurun_out/golden/log_$c.txt 2>&1
     echo "rc $?" >> gpurun_out/golden/log_$c.txt
   done ) &
 FIX=$!
