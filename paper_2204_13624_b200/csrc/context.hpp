@@ -113,7 +113,9 @@ struct FftPlan {
   // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
   // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off
   bool zbulk = false;  // z-inverse with spectrum rows staged per block (COMBO_ZBULK=1; measured slower: 2 blocks/SM)
-  bool zring = true;  // persistent ring-staged z-inverse at n3 = 512 (COMBO_ZRING=0: one block per tile)
+  // persistent ring-staged z-inverse at n3 = 512: consumer groups (COMBO_ZRING = 2 / 3; 0: one block per
+  // tile) and who prefetches the consumer's rows (COMBO_ZRING_PF, see zinv_ring)
+  int zring = 2, zring_pf = 1;
   bool tma_x = false, tma_y = false;
   int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
   CUtensorMap xmap{}, ymap{};

@@ -246,7 +246,8 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->xminb = knob("COMBO_XMINB", 2);
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
-  p->zring = knob("COMBO_ZRING", 1) != 0;
+  p->zring = knob("COMBO_ZRING", 2);
+  p->zring_pf = knob("COMBO_ZRING_PF", 1);
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -578,17 +579,23 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
       const size_t rows = size_t(9 * p.rzL) * size_t(p.n3p) * sizeof(double2);
       bool ring = false;
       if constexpr (L == 9) {
-        // persistent ring-staged kernel: one z-line per tile, two consumer groups
-        using Z = combo_dev::ZRing<L>;
-        const int stages = int(std::min<size_t>(4, (227 * 1024 - Z::kHead - 2 * Z::kWork) / rows));
-        if (p.zring && p.rzL == 1 && stages >= 2) {
-          const size_t smem = size_t(Z::kHead + 2 * Z::kWork) + size_t(stages) * rows;
-          auto k = zinv_ring<Cons, L>;
+        // persistent ring-staged kernel: one z-line per tile, NG consumer groups
+        auto go = [&](auto ngc) {
+          constexpr int NG = decltype(ngc)::value;
+          using Z = combo_dev::ZRing<L, NG>;
+          const int stages = int(std::min<size_t>(4, (227 * 1024 - Z::kHead - NG * Z::kWork) / rows));
+          if (stages < 2) return;
+          const size_t smem = size_t(Z::kHead + NG * Z::kWork) + size_t(stages) * rows;
+          auto k = zinv_ring<Cons, L, NG>;
           smem_attr(k, smem);
           const int grid = int(std::min<int64_t>(nb, c->num_sms));
-          k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, scale, cons, part, stages);
+          k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, scale, cons, part, stages, p.zring_pf);
           ring = true;
-        }
+        };
+        if (p.zring == 3 && p.rzL == 1)
+          go(std::integral_constant<int, 3>{});
+        else if (p.zring == 2 && p.rzL == 1)
+          go(std::integral_constant<int, 2>{});
       }
       if (ring) {
       } else if (p.zbulk && p.rzsmem % 128 == 0 && p.rzsmem + rows <= 100 * 1024) {

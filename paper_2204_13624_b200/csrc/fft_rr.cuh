@@ -508,23 +508,26 @@ static __global__ void __launch_bounds__(512, 2)
 // per tile): one block per SM; a producer lane streams the 9 spectrum rows
 // of each tile into a ring of shared-memory stages with cp.async.bulk (and
 // L2-prefetches the consumer's field rows); two consumer groups of
-// 5 N/8 threads take alternate tiles -- Hermitian completion from the stage
+// 5 N/8 threads (NG = 2 or 3) take tiles in turn -- Hermitian completion from the stage
 // into the group's pair lines, inverse stages with a named barrier over the
 // group, consumer epilogue -- so the completion / transform / epilogue phases
 // of one tile overlap the other group's and the loads of the next tiles.
 // Partials are indexed by tile: same values and order as zinv_rr.
-template <int L>
+template <int L, int NG>
 struct ZRing {
   static constexpr int N = 1 << L, LS = N + N / 8, NP = 5, GT = NP * (N / 8);  // threads per consumer group
   static constexpr int kHead = 128;
   static constexpr int kWork = NP * LS * 16;  // pair lines of one group
-  static constexpr int kThreads = 2 * GT + 32;
+  static constexpr int kThreads = NG * GT + 32;
 };
 
-template <class Cons, int L>
-static __global__ void __launch_bounds__(ZRing<L>::kThreads, 1)
-    zinv_ring(SpecView sv, const double2* __restrict__ tw, double scale, Cons cons, double* partials, int nstages) {
-  using Z = ZRing<L>;
+// pf: who L2-prefetches the consumer's field rows -- 0 nobody, 1 the
+// producer with the tile's loads, 2 each consumer group for its next tile
+template <class Cons, int L, int NG>
+static __global__ void __launch_bounds__(ZRing<L, NG>::kThreads, 1)
+    zinv_ring(SpecView sv, const double2* __restrict__ tw, double scale, Cons cons, double* partials, int nstages,
+              int pf) {
+  using Z = ZRing<L, NG>;
   constexpr int N = Z::N, LS = Z::LS, NP = Z::NP, GT = Z::GT;
   extern __shared__ __align__(128) unsigned char zr_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(zr_raw);
@@ -532,7 +535,7 @@ static __global__ void __launch_bounds__(ZRing<L>::kThreads, 1)
   const int n3p = int(sv.n3p), nc = int(sv.n3c);
   const int ncr = (nc + 31) & ~31;  // warp-aligned k ranges (see zfwd_rr)
   const uint32_t stage_bytes = uint32_t(9 * n3p) * 16u;
-  unsigned char* stages = zr_raw + Z::kHead + 2 * Z::kWork;
+  unsigned char* stages = zr_raw + Z::kHead + NG * Z::kWork;
   const int64_t ntiles = sv.ni * sv.n2;  // local z-lines
   if (threadIdx.x == 0) {
     for (int s = 0; s < nstages; ++s) {
@@ -542,7 +545,7 @@ static __global__ void __launch_bounds__(ZRing<L>::kThreads, 1)
     mbar_fence_init();
   }
   __syncthreads();
-  if (int(threadIdx.x) >= 2 * GT) {  // producer warp
+  if (int(threadIdx.x) >= NG * GT) {  // producer warp
     if ((threadIdx.x & 31) == 0) {
       Ring rg(nstages);
       int k = 0;
@@ -553,8 +556,10 @@ static __global__ void __launch_bounds__(ZRing<L>::kThreads, 1)
         mbar_expect_tx(&full[rg.s], 9u * rb);
 #pragma unroll 1
         for (int rl = 0; rl < 9; ++rl) bulk_g2s(rows + rl * n3p, sv.spec + sv.zrow(rl, tile), rb, &full[rg.s]);
+        if (pf == 1) {
 #pragma unroll 1
-        for (int c = 0; c < 9; ++c) cons.prefetch(c, tile * N, N);
+          for (int c = 0; c < 9; ++c) cons.prefetch(c, tile * N, N);
+        }
       }
     }
     return;
@@ -565,7 +570,11 @@ static __global__ void __launch_bounds__(ZRing<L>::kThreads, 1)
   Ring rg(nstages);
   int k = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k, rg.next()) {
-    if ((k & 1) != g) continue;
+    if (k % NG != g) continue;
+    if (pf == 2 && tid < 9) {
+      const int64_t nxt = tile + int64_t(NG) * gridDim.x;
+      if (nxt < ntiles) cons.prefetch(tid, nxt * N, N);
+    }
     gsync();  // the previous tile's reduction has left the pair lines
     mbar_wait(&full[rg.s], rg.phase);
     const double2* rows = reinterpret_cast<const double2*>(stages + size_t(rg.s) * stage_bytes);

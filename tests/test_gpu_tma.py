@@ -76,7 +76,8 @@ def test_zinv_staged_variants_bitwise_equal_register_loads(dims):
     rng = np.random.default_rng(21)
     tau = rng.uniform(-1, 1, 9 * int(np.prod(dims)))
     outs = []
-    for knobs in (dict(COMBO_ZRING=1), dict(COMBO_ZRING=0, COMBO_ZBULK=0), dict(COMBO_ZRING=0, COMBO_ZBULK=1)):
+    for knobs in (dict(COMBO_ZRING=2), dict(COMBO_ZRING=0, COMBO_ZBULK=0), dict(COMBO_ZRING=0, COMBO_ZBULK=1),
+                  dict(COMBO_ZRING=3, COMBO_ZRING_PF=2)):
         c, old = _fresh_ctx(**knobs)
         try:
             outs.append(c.project(tau, "rotated", dims, (1, 1, 1)))
@@ -100,7 +101,7 @@ def test_zinv_ring_solve_bitwise(oracle, scheme, green):
     fbar[0, 0] += 0.04
     fbar[0, 1] += 0.02
     runs = []
-    for ring in (1, 0):
+    for ring in (2, 0, 3):
         c, old = _fresh_ctx(COMBO_ZRING=ring)
         try:
             img = c.generate("rsa_spheres", fine, (1, 1, 1), 3, 3.0, 6.0, 0.3)
@@ -112,12 +113,13 @@ def test_zinv_ring_solve_bitwise(oracle, scheme, green):
         finally:
             _restore(old)
             c.close()
-    (a, grid), (b, _) = runs
-    assert a["report"]["success"] and b["report"]["success"]
-    for sa, sb in zip(a["report"]["steps"], b["report"]["steps"]):
-        assert sa["cg_iters"] == sb["cg_iters"] and sa["residuals"] == sb["residuals"]
-        assert sa["pbar_history"] == sb["pbar_history"]
-    assert np.array_equal(a["f"].view(np.uint64), b["f"].view(np.uint64))
+    (a, grid) = runs[0]
+    for b, _ in runs[1:]:
+        assert a["report"]["success"] and b["report"]["success"]
+        for sa, sb in zip(a["report"]["steps"], b["report"]["steps"]):
+            assert sa["cg_iters"] == sb["cg_iters"] and sa["residuals"] == sb["residuals"]
+            assert sa["pbar_history"] == sb["pbar_history"]
+        assert np.array_equal(a["f"].view(np.uint64), b["f"].view(np.uint64))
     kind, cp, nrm = grid
     cmo = oracle.CellMaterials(dims, kind, cp, nrm, oracle.neo_hookean(2.0, 1.0), oracle.neo_hookean(20.0, 10.0))
     ro = cmo.solve(fbar, scheme=1 if scheme == "newton_cg" else 0, green={"rotated": 1, "continuous": 0}[green],
