@@ -146,8 +146,9 @@ def workload(gpus, mode):
     return c5_ladder(gpus) if mode == "weak" else CONFIGS["C5"]
 
 
-def first_increment(cfg):
-    return np.eye(3) + (cfg.fbar - np.eye(3)) / cfg.load_steps
+def first_increment(cfg, k=1):
+    """macroscopic F after the first k of the config's load increments"""
+    return np.eye(3) + k * (cfg.fbar - np.eye(3)) / cfg.load_steps
 
 
 def ls_counts(report):
@@ -264,6 +265,8 @@ def main():
     ap.add_argument("--check", action="store_true", help="strong mode: bitwise check against one GPU")
     ap.add_argument("--cpu-ls", type=int, default=2, help="timed LS iterations of the cpu_baseline leg")
     ap.add_argument("--cpu-leg", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--increments", type=int, default=1,
+                    help="load increments of the config per bench step (default: the first; C5 has 5)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -328,8 +331,9 @@ def main():
         dist.all_reduce(t)
         ncomp = float(t.item())
     phi = ncomp / N
-    fbar = first_increment(cfg)
-    kw = dict(scheme=cfg.scheme, green=cfg.green, tol_equilibrium=cfg.tol, max_outer=cfg.max_outer, load_steps=1)
+    fbar = first_increment(cfg, args.increments)
+    kw = dict(scheme=cfg.scheme, green=cfg.green, tol_equilibrium=cfg.tol, max_outer=cfg.max_outer,
+              load_steps=args.increments)
 
     def step():
         cm.reset_warm_starts()
@@ -421,6 +425,11 @@ def main():
     if rank == 0:
         rep0 = reports[-1]
         cfgd = config_dict(cfg, world, args.mode)
+        if args.increments > 1:
+            cfgd["workload"] = cfgd["workload"].replace("first load increment",
+                                                        f"first {args.increments} load increments")
+            cfgd["ls_per_increment"] = [s["ls_residual"] + s["ls_cg"] + s["ls_trial"] + s["ls_basic"]
+                                        for s in rep0["steps"]]
         cfgd.update({"composite_fraction": phi, "ls_per_step": ls_total / args.steps, "ls_mix": counts,
                      "newton_per_step": sum(s["outer_iters"] for s in rep0["steps"]), "preprocess_s": t_pre,
                      "preprocess": "per-slab device generation / coarsening / normals" if world > 1

@@ -110,12 +110,14 @@ struct FftPlan {
   bool mv_bulk = true;  // bulk-staged CG matvec (COMBO_MV_BULK=0: one cell per thread, direct loads)
   bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
+  bool pq_dot = true;    // CG: pdir^T A pdir summed in the matvec (COMBO_PQ=0: in the z-inverse consumer)
   // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
   // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off
   bool zbulk = false;  // z-inverse with spectrum rows staged per block (COMBO_ZBULK=1; measured slower: 2 blocks/SM)
   // persistent ring-staged z-inverse at n3 = 512: consumer groups (COMBO_ZRING = 2 / 3; 0: one block per
   // tile) and who prefetches the consumer's rows (COMBO_ZRING_PF, see zinv_ring)
   int zring = 2, zring_pf = 1;
+  int zfring = 2;  // persistent ring-staged z-forward at n3 = 512: consumer groups (COMBO_ZFRING = 2 / 3; 0: off)
   bool tma_x = false, tma_y = false;
   int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
   CUtensorMap xmap{}, ymap{};

@@ -246,8 +246,10 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->xminb = knob("COMBO_XMINB", 2);
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
+  p->pq_dot = knob("COMBO_PQ", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
   p->zring_pf = knob("COMBO_ZRING_PF", 1);
+  p->zfring = knob("COMBO_ZFRING", 2);
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -509,8 +511,8 @@ template <bool FIRST, bool HASX>
 void launch_matvec_bulk(combo_ctx* c, const MatvecArgs& a, double* q) {
   using S = combo_dev::MvStage<FIRST, HASX>;
   constexpr int kMaxSmem = 227 * 1024;
-  const int stages = std::min(4, (kMaxSmem - 128) / S::kBytes);
-  const size_t smem = 128 + size_t(stages) * S::kBytes;
+  const int stages = std::min(4, (kMaxSmem - combo_dev::kMvHead) / S::kBytes);
+  const size_t smem = combo_dev::kMvHead + size_t(stages) * S::kBytes;
   auto kern = combo_dev::k_matvec_bulk<FIRST, HASX>;
   static bool attr = false;  // per instantiation
   if (!attr) {
@@ -522,10 +524,14 @@ void launch_matvec_bulk(combo_ctx* c, const MatvecArgs& a, double* q) {
   kern<<<grid, combo_dev::kMvT + 32, smem, c->stream>>>(a, q, stages);
 }
 
-void launch_matvec(combo_ctx* c, const MatvecArgs& a, double* q) {
+bool mv_bulk_ok(const combo_ctx* c, const MatvecArgs& a) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  const bool bulk = c->plan && c->plan->mv_bulk && a.N % 2 == 0 && al16(a.r) && al16(a.fin) && al16(a.pdir) &&
-                    (a.xv == nullptr || al16(a.xv)) && al16(a.cd.cid);
+  return c->plan && c->plan->mv_bulk && a.N % 2 == 0 && al16(a.r) && al16(a.fin) && al16(a.pdir) &&
+         (a.xv == nullptr || al16(a.xv)) && al16(a.cd.cid);
+}
+
+void launch_matvec(combo_ctx* c, const MatvecArgs& a, double* q) {
+  const bool bulk = mv_bulk_ok(c, a);
   if (!bulk) {
     combo_dev::k_matvec<><<<ew_grid(a.N), kEwThreads, 0, c->stream>>>(a, q);
     return;
@@ -543,6 +549,30 @@ int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
   FftPlan& p = *c->plan;
   int64_t nb = 0;
   ProfScope ps(c, Prod::CELL ? kTagMvZfwd : kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
+  if constexpr (std::is_same_v<Prod, ProdLoad9>) {
+    // persistent ring-staged kernel (z-lines of 512 cells, 16-byte aligned field)
+    if (p.dims[2] == 512 && p.zfring >= 2 && (reinterpret_cast<uintptr_t>(prod.src) & 15) == 0) {
+      auto go = [&](auto ngc) {
+        constexpr int NG = decltype(ngc)::value;
+        using Z = combo_dev::ZRing<9, NG>;
+        const size_t stage = 9 * 512 * 8, head = size_t(Z::kHead) + NG * size_t(Z::kWork + 128);
+        const int stages = int(std::min<size_t>(4, (227 * 1024 - head) / stage));
+        const size_t smem = head + size_t(stages) * stage;
+        auto k = zfwd_ring<9, NG>;
+        smem_attr(k, smem);
+        nb = p.ni * p.dims[1];
+        const int grid = int(std::min<int64_t>(nb, c->num_sms));
+        k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, prod.src, prod.N, stages);
+      };
+      if (p.zfring == 3)
+        go(std::integral_constant<int, 3>{});
+      else
+        go(std::integral_constant<int, 2>{});
+      ++c->launches;
+      COMBO_CK(cudaGetLastError());
+      return nb;
+    }
+  }
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
@@ -1215,6 +1245,11 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
     axpy_x(step_prev);
   };
   auto cons = [&](size_t k) { return ConsCg{P(ap_, k), P(pd_, k), rk_[k].N}; };
+  // pdir^T A pdir taken in the matvec as pdir . q (see MatvecArgs::pq_part):
+  // the z-inverse then only stores ap and never reads pdir. Needs the bulk
+  // matvec and tiles that do not straddle planes (decomposition invariance).
+  bool pq = !dfmg && c_->plan->pq_dot && !c_->plan->fuse_mv && (c_->dims[1] * c_->dims[2]) % combo_dev::kMvT == 0;
+  const int64_t ntiles = c_->N / combo_dev::kMvT;
   while (it < cfg_.cg_max) {
     count_ls();
     ++rep.ls_cg;
@@ -1228,8 +1263,10 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
       auto mv = [&](size_t k) {
         combo_ctx* m = rk_[k].c;
         return ProdMatvec{{m->mp, m->cell_data(), P(F_, k), shF_, P(r_, k), P(pd_, k), beta, it == 0 ? 1 : 0,
-                           rk_[k].N, P(x_, k), step_prev}};
+                           rk_[k].N, P(x_, k), step_prev, nullptr}};
       };
+      if (pq)
+        for (size_t k = 0; k < rk_.size(); ++k) pq = pq && mv_bulk_ok(rk_[k].c, mv(k).a);
       const double mvb = (it == 0 ? 220.0 : 436.0) * double(c_->N) + 360.0 * double(c_->ncomp);
       if (c_->plan->fuse_mv) {
         project_group(c_, cfg_.green, mv, cons, 20, mvb);
@@ -1237,13 +1274,21 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
         for (size_t k = 0; k < rk_.size(); ++k) {
           combo_ctx* m = rk_[k].c;
           ProfScope ps(m, kTagMatvec, mvb + 72.0 * double(rk_[k].N));
-          const MatvecArgs a = mv(k).a;
+          MatvecArgs a = mv(k).a;
+          if (pq) a.pq_part = part_ptr(m, ntiles, 1);
           launch_matvec(m, a, P(rb_, k));
           ++m->launches;
           COMBO_CK(cudaGetLastError());
         }
-        project_group(
-            c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; }, cons, 20);
+        if (pq) {
+          group_reduce(c_, ntiles, 1, 20);
+          project_group(
+              c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
+              [&](size_t k) { return ConsStore9{P(ap_, k), rk_[k].N}; }, 20);
+        } else {
+          project_group(
+              c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; }, cons, 20);
+        }
       }
     }
     fetch_results(c_, false);

@@ -359,6 +359,10 @@ struct MatvecArgs {
   int64_t N;
   double* xv;
   double step_prev;
+  // bulk kernel only: per-tile sums of pdir . q (pdir^T A pdir; equals
+  // pdir^T Pi(q) of solver.cpp:181 because pdir lies in the range of the
+  // self-adjoint projection Pi), one value per kMvT-cell tile; may be null
+  double* pq_part;
 };
 
 __device__ __forceinline__ void mv_cell(const MatvecArgs& a, int64_t cell, double* y) {
@@ -419,6 +423,7 @@ static __global__ void __launch_bounds__(kEwThreads, MINB) k_matvec(MatvecArgs a
 // memory and store pdir, x and q. Cells past the last full tile are done by
 // block 0 with direct loads. Requires N even and 16-byte aligned rows.
 constexpr int kMvT = 256;
+constexpr int kMvHead = 256;  // barriers + reduction slots ahead of the ring
 
 template <bool FIRST, bool HASX>
 struct MvStage {
@@ -433,7 +438,8 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + 8;
-  unsigned char* buf = smem_raw + 128;
+  double* red = reinterpret_cast<double*>(smem_raw + 128);  // [2][8] warp sums of pdir . q
+  unsigned char* buf = smem_raw + kMvHead;
   const int64_t N = a.N;
   const int64_t nfull = N / kMvT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,6 +475,7 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
   }
   const int tid = threadIdx.x;
   Ring rg(nstages);
+  int par = 0;
   for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x, rg.next()) {
     mbar_wait(&full[rg.s], rg.phase);
     const double* d = reinterpret_cast<const double*>(buf + size_t(rg.s) * S::kBytes);
@@ -506,6 +513,23 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
     if (lane == 0) mbar_arrive(&empty[rg.s]);
 #pragma unroll
     for (int c = 0; c < 9; ++c) q[c * N + cell] = y[c];
+    if (a.pq_part) {
+      // fixed-order tile sum: 9 products per cell, warp tree, 8 warp sums
+      double dq = 0.0;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) dq += x[c] * y[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dq += __shfl_down_sync(0xffffffffu, dq, o);
+      if (lane == 0) red[par * 8 + warp] = dq;
+      asm volatile("bar.sync 1, %0;" ::"n"(kMvT) : "memory");
+      if (tid == 0) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kMvT / 32; ++w) sum += red[par * 8 + w];
+        a.pq_part[t] = sum;
+      }
+      par ^= 1;
+    }
   }
   if (blockIdx.x == 0) {
     for (int64_t cell = nfull * kMvT + tid; cell < N; cell += kMvT) {
