@@ -114,10 +114,10 @@ struct FftPlan {
   // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
   // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off
   bool zbulk = false;  // z-inverse with spectrum rows staged per block (COMBO_ZBULK=1; measured slower: 2 blocks/SM)
-  // persistent ring-staged z-inverse at n3 = 512: consumer groups (COMBO_ZRING = 2 / 3; 0: one block per
-  // tile) and who prefetches the consumer's rows (COMBO_ZRING_PF, see zinv_ring)
-  int zring = 2, zring_pf = 1;
-  int zfring = 2;  // persistent ring-staged z-forward at n3 = 512: consumer groups (COMBO_ZFRING = 2 / 3; 0: off)
+  // persistent ring-staged z passes at n3 = 512 (two consumer groups; COMBO_ZRING / COMBO_ZFRING = 0: one
+  // block per tile); the z-inverse uses it for consumers whose epilogue reads no field (Cons::LOADS)
+  int zring = 2, zring_pf = 0;
+  int zfring = 2;
   bool tma_x = false, tma_y = false;
   int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
   CUtensorMap xmap{}, ymap{};

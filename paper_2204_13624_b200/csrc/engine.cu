@@ -248,7 +248,7 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
-  p->zring_pf = knob("COMBO_ZRING_PF", 1);
+  p->zring_pf = knob("COMBO_ZRING_PF", 0);
   p->zfring = knob("COMBO_ZFRING", 2);
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
@@ -564,10 +564,7 @@ int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
         const int grid = int(std::min<int64_t>(nb, c->num_sms));
         k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, prod.src, prod.N, stages);
       };
-      if (p.zfring == 3)
-        go(std::integral_constant<int, 3>{});
-      else
-        go(std::integral_constant<int, 2>{});
+      go(std::integral_constant<int, 2>{});
       ++c->launches;
       COMBO_CK(cudaGetLastError());
       return nb;
@@ -614,7 +611,7 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
           constexpr int NG = decltype(ngc)::value;
           using Z = combo_dev::ZRing<L, NG>;
           const int stages = int(std::min<size_t>(4, (227 * 1024 - Z::kHead - NG * Z::kWork) / rows));
-          if (stages < 2) return;
+          if (stages < NG + 1) return;  // a group may run at most one ring phase ahead
           const size_t smem = size_t(Z::kHead + NG * Z::kWork) + size_t(stages) * rows;
           auto k = zinv_ring<Cons, L, NG>;
           smem_attr(k, smem);
@@ -622,10 +619,7 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
           k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, scale, cons, part, stages, p.zring_pf);
           ring = true;
         };
-        if (p.zring == 3 && p.rzL == 1)
-          go(std::integral_constant<int, 3>{});
-        else if (p.zring == 2 && p.rzL == 1)
-          go(std::integral_constant<int, 2>{});
+        if (p.zring >= 2 && p.rzL == 1 && !Cons::LOADS) go(std::integral_constant<int, 2>{});
       }
       if (ring) {
       } else if (p.zbulk && p.rzsmem % 128 == 0 && p.rzsmem + rows <= 100 * 1024) {

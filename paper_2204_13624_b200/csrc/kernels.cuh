@@ -749,6 +749,7 @@ struct ConsStore9 {
   static constexpr int NSC = 0;
   static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 1;
+  static constexpr bool LOADS = false;  // the epilogue reads fields (ring kernel: latency exposed)
   double* dst;
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, const double* v, double*) const {
@@ -767,6 +768,7 @@ struct ConsStore9 {
 struct ConsBasic {
   static constexpr int NRED = 10;
   static constexpr int FIELDS = 2;
+  static constexpr bool LOADS = true;  // the epilogue reads fields (ring kernel: latency exposed)
   const double* fold;
   Shift9 fold_shift;
   double* fnew;
@@ -804,6 +806,7 @@ struct ConsResid {
   static constexpr int NSC = 1;
   static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 1;
+  static constexpr bool LOADS = false;  // the epilogue reads fields (ring kernel: latency exposed)
   double* r;
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
@@ -827,6 +830,7 @@ struct ConsCg {
   static constexpr int NSC = 1;
   static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 2;
+  static constexpr bool LOADS = true;  // the epilogue reads fields (ring kernel: latency exposed)
   double* ap;
   const double* pdir;
   int64_t N;

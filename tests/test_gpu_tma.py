@@ -77,7 +77,7 @@ def test_zinv_staged_variants_bitwise_equal_register_loads(dims):
     tau = rng.uniform(-1, 1, 9 * int(np.prod(dims)))
     outs = []
     for knobs in (dict(COMBO_ZRING=2, COMBO_ZFRING=2), dict(COMBO_ZRING=0, COMBO_ZBULK=0, COMBO_ZFRING=0),
-                  dict(COMBO_ZRING=0, COMBO_ZBULK=1, COMBO_ZFRING=3), dict(COMBO_ZRING=3, COMBO_ZRING_PF=2)):
+                  dict(COMBO_ZRING=0, COMBO_ZBULK=1, COMBO_ZFRING=2), dict(COMBO_ZRING=2, COMBO_ZFRING=0)):
         c, old = _fresh_ctx(**knobs)
         try:
             outs.append(c.project(tau, "rotated", dims, (1, 1, 1)))
@@ -101,7 +101,7 @@ def test_zinv_ring_solve_bitwise(oracle, scheme, green):
     fbar[0, 0] += 0.04
     fbar[0, 1] += 0.02
     runs = []
-    for ring in (2, 0, 3):
+    for ring in (2, 0):
         c, old = _fresh_ctx(COMBO_ZRING=ring, COMBO_ZFRING=ring)
         try:
             img = c.generate("rsa_spheres", fine, (1, 1, 1), 3, 3.0, 6.0, 0.3)
