@@ -111,13 +111,13 @@ struct FftPlan {
   bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
   bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
   bool pq_dot = true;    // CG: pdir^T A pdir summed in the matvec (COMBO_PQ=0: in the z-inverse consumer)
+  bool r_defer = true;   // CG: r update deferred into the next matvec, r^T r by recurrence (COMBO_RDEFER=0)
   // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
   // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off
   bool zbulk = false;  // z-inverse with spectrum rows staged per block (COMBO_ZBULK=1; measured slower: 2 blocks/SM)
-  // persistent ring-staged z passes at n3 = 512 (two consumer groups; COMBO_ZRING / COMBO_ZFRING = 0: one
-  // block per tile); the z-inverse uses it for consumers whose epilogue reads no field (Cons::LOADS)
+  // persistent ring-staged z-inverse at n3 = 512 (two consumer groups; COMBO_ZRING=0: one block per
+  // tile), used for consumers whose epilogue reads no field (Cons::LOADS)
   int zring = 2, zring_pf = 0;
-  int zfring = 2;
   bool tma_x = false, tma_y = false;
   int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
   CUtensorMap xmap{}, ymap{};
@@ -216,6 +216,7 @@ struct combo_ctx {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t pipe_ev[12] = {nullptr};
   combo_host::DBuf<double> gpart;              // leader: block partials of all ranks
+  combo_host::DBuf<double> gpart2;             // leader: chunk sums of long partial vectors
   combo_host::DBuf<combo_dev::Stats> gstats;   // NCCL: laminate stats of all ranks
   std::unique_ptr<combo_host::FftPlan> plan;
 

@@ -247,9 +247,9 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
+  p->r_defer = knob("COMBO_RDEFER", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
   p->zring_pf = knob("COMBO_ZRING_PF", 0);
-  p->zfring = knob("COMBO_ZFRING", 2);
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -369,9 +369,31 @@ Stats* stats_ptr(combo_ctx* c) { return leader(c)->dstats.p; }
 // fixed-order combination of every rank's block partials -> dres[slot..]
 void group_reduce(combo_ctx* c, int64_t nb, int nred, int slot) {
   combo_ctx* L = leader(c);
-  if (L->nccl && L->R > 1) nccl_allgather_inplace(L, L->gpart.p, size_t(nb) * size_t(nred));
+  const int64_t total = int64_t(L->R) * nb;
+  constexpr int kChunkRed = 4096;
+  const bool two_level = total > (int64_t(1) << 20);
+  // long vectors (the matvec's per-warp sums): sums over fixed chunks of the
+  // global block order first. Chunks that do not straddle ranks are summed
+  // by their owner, so only the chunk sums cross NVLink.
+  const bool local_chunks = two_level && nb % kChunkRed == 0;
+  if (L->nccl && L->R > 1 && !local_chunks) nccl_allgather_inplace(L, L->gpart.p, size_t(nb) * size_t(nred));
   ProfScope ps(L, kTagReduce, double(L->R) * double(nb) * nred * 8.0);
-  k_reduce_partials<<<nred, 1024, 0, L->stream>>>(L->gpart.p, int64_t(L->R) * nb, nred, L->dres.p + slot);
+  if (two_level) {
+    const int64_t nch = (total + kChunkRed - 1) / kChunkRed;
+    if (L->gpart2.n < size_t(nch * nred)) L->gpart2.alloc(size_t(nch * nred));
+    if (L->nccl && L->R > 1 && local_chunks) {
+      const int64_t nloc = nb / kChunkRed;
+      k_reduce_chunks<<<unsigned(nloc), 256, 0, L->stream>>>(L->gpart.p + size_t(L->q) * size_t(nb) * nred, nb, nred,
+                                                            kChunkRed, L->gpart2.p + size_t(L->q) * size_t(nloc) * nred);
+      nccl_allgather_inplace(L, L->gpart2.p, size_t(nloc) * size_t(nred));
+    } else {
+      k_reduce_chunks<<<unsigned(nch), 256, 0, L->stream>>>(L->gpart.p, total, nred, kChunkRed, L->gpart2.p);
+    }
+    k_reduce_partials<<<nred, 1024, 0, L->stream>>>(L->gpart2.p, nch, nred, L->dres.p + slot);
+    ++L->launches;
+  } else {
+    k_reduce_partials<<<nred, 1024, 0, L->stream>>>(L->gpart.p, total, nred, L->dres.p + slot);
+  }
   ++L->launches;
   COMBO_CK(cudaGetLastError());
 }
@@ -507,13 +529,13 @@ int ahead_blocks(const combo_ctx* c, K kernel, int threads, size_t smem) {
 
 // CG matvec: bulk-staged persistent kernel (one CTA per SM) when the rows
 // are 16-byte aligned, else one cell per thread with direct loads.
-template <bool FIRST, bool HASX>
+template <bool FIRST, bool HASX, bool RUPD = false>
 void launch_matvec_bulk(combo_ctx* c, const MatvecArgs& a, double* q) {
   using S = combo_dev::MvStage<FIRST, HASX>;
   constexpr int kMaxSmem = 227 * 1024;
   const int stages = std::min(4, (kMaxSmem - combo_dev::kMvHead) / S::kBytes);
   const size_t smem = combo_dev::kMvHead + size_t(stages) * S::kBytes;
-  auto kern = combo_dev::k_matvec_bulk<FIRST, HASX>;
+  auto kern = combo_dev::k_matvec_bulk<FIRST, HASX, RUPD>;
   static bool attr = false;  // per instantiation
   if (!attr) {
     COMBO_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -538,6 +560,8 @@ void launch_matvec(combo_ctx* c, const MatvecArgs& a, double* q) {
   }
   if (a.first)
     launch_matvec_bulk<true, false>(c, a, q);
+  else if (a.xv && a.ap)
+    launch_matvec_bulk<false, true, true>(c, a, q);
   else if (a.xv)
     launch_matvec_bulk<false, true>(c, a, q);
   else
@@ -549,27 +573,6 @@ int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
   FftPlan& p = *c->plan;
   int64_t nb = 0;
   ProfScope ps(c, Prod::CELL ? kTagMvZfwd : kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
-  if constexpr (std::is_same_v<Prod, ProdLoad9>) {
-    // persistent ring-staged kernel (z-lines of 512 cells, 16-byte aligned field)
-    if (p.dims[2] == 512 && p.zfring >= 2 && (reinterpret_cast<uintptr_t>(prod.src) & 15) == 0) {
-      auto go = [&](auto ngc) {
-        constexpr int NG = decltype(ngc)::value;
-        using Z = combo_dev::ZRing<9, NG>;
-        const size_t stage = 9 * 512 * 8, head = size_t(Z::kHead) + NG * size_t(Z::kWork + 128);
-        const int stages = int(std::min<size_t>(4, (227 * 1024 - head) / stage));
-        const size_t smem = head + size_t(stages) * stage;
-        auto k = zfwd_ring<9, NG>;
-        smem_attr(k, smem);
-        nb = p.ni * p.dims[1];
-        const int grid = int(std::min<int64_t>(nb, c->num_sms));
-        k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, prod.src, prod.N, stages);
-      };
-      go(std::integral_constant<int, 2>{});
-      ++c->launches;
-      COMBO_CK(cudaGetLastError());
-      return nb;
-    }
-  }
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
@@ -1243,7 +1246,11 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
   // the z-inverse then only stores ap and never reads pdir. Needs the bulk
   // matvec and tiles that do not straddle planes (decomposition invariance).
   bool pq = !dfmg && c_->plan->pq_dot && !c_->plan->fuse_mv && (c_->dims[1] * c_->dims[2]) % combo_dev::kMvT == 0;
-  const int64_t ntiles = c_->N / combo_dev::kMvT;
+  const int64_t ntiles = (c_->N / combo_dev::kMvT) * (combo_dev::kMvT / 32);  // per-warp sums
+  // ... and the residual update deferred into the next matvec, r^T r by the
+  // recurrence rr' = rr - 2 s (r . q) + s^2 |ap|^2 (r . ap = r . q as above)
+  // whenever it loses at most 4 digits; else the direct update (k_cg_update)
+  double rstep = 0.0;
   while (it < cfg_.cg_max) {
     count_ls();
     ++rep.ls_cg;
@@ -1267,14 +1274,26 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
       } else {
         for (size_t k = 0; k < rk_.size(); ++k) {
           combo_ctx* m = rk_[k].c;
-          ProfScope ps(m, kTagMatvec, mvb + 72.0 * double(rk_[k].N));
+          const bool rdef = pq && c_->plan->r_defer;
+          // + q write; deferred residual update: + ap read, r write
+          ProfScope ps(m, kTagMatvec, mvb + (rdef && it > 0 ? 216.0 : 72.0) * double(rk_[k].N));
           MatvecArgs a = mv(k).a;
-          if (pq) a.pq_part = part_ptr(m, ntiles, 1);
+          if (pq) a.pq_part = part_ptr(m, ntiles, rdef && it > 0 ? 2 : 1);
+          if (rdef && it > 0) {
+            a.ap = P(ap_, k);
+            a.rstep = rstep;
+            a.r_out = P(r_, k);
+          }
           launch_matvec(m, a, P(rb_, k));
           ++m->launches;
           COMBO_CK(cudaGetLastError());
         }
-        if (pq) {
+        if (pq && c_->plan->r_defer) {
+          group_reduce(c_, ntiles, it > 0 ? 2 : 1, 20);  // pdir . q (, r . q) -> 20 (, 21)
+          project_group(
+              c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
+              [&](size_t k) { return ConsStoreAA{P(ap_, k), rk_[k].N}; }, 22);  // |ap|^2 -> 22
+        } else if (pq) {
           group_reduce(c_, ntiles, 1, 20);
           project_group(
               c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
@@ -1295,6 +1314,24 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
     }
     const double step = rr / pap;
     if (dfmg) axpy_x(step);
+    if (pq && c_->plan->r_defer) {
+      // first iteration: pdir = r, so r . q = pdir . q
+      const double rq = it > 0 ? c_->hres[21] : pap;
+      const double rr_rec = rr - 2.0 * step * rq + step * step * c_->hres[22];
+      if (rr_rec >= 1e-4 * rr) {
+        rstep = step;
+        ++it;
+        step_prev = step;
+        if (std::sqrt(rr_rec) <= tol_rel * bnorm) {
+          flush_x();
+          return it;
+        }
+        beta = rr_rec / rr;
+        rr = rr_rec;
+        continue;
+      }
+      rstep = 0.0;  // strong cancellation: update r and take its norm directly below
+    }
     for (auto& r : rk_) {
       double* part = part_ptr(r.c, nbc, 1);
       ProfScope ps(r.c, kTagCgUpdate, 216.0 * double(r.N));

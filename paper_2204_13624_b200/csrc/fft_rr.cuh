@@ -599,89 +599,6 @@ static __global__ void __launch_bounds__(ZRing<L, NG>::kThreads, 1)
   }
 }
 
-// Persistent ring-staged z-forward of a stored field (ProdLoad9) for z-lines
-// of 512 cells, the mirror image of zinv_ring: the producer lane streams the
-// 9 real lines of each tile (4 KB each) into the ring; a consumer group
-// packs pairs of lines into complex lines on its first-stage read, runs the
-// stages in its own pair-line buffer, splits the pairs and stores the 9
-// half-spectrum rows. Same arithmetic as zfwd_rr (bitwise).
-template <int L, int NG>
-static __global__ void __launch_bounds__(ZRing<L, NG>::kThreads, 1)
-    zfwd_ring(SpecView sv, const double2* __restrict__ tw, const double* __restrict__ src, int64_t Nf, int nstages) {
-  using Z = ZRing<L, NG>;
-  constexpr int N = Z::N, LS = Z::LS, NP = Z::NP, GT = Z::GT, TL = N / 8;
-  constexpr int kGroup = Z::kWork + 128;  // pair lines + spectrum row offsets
-  extern __shared__ __align__(128) unsigned char zr_raw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(zr_raw);
-  uint64_t* empty = full + 8;
-  constexpr uint32_t stage_bytes = 9u * N * 8u;
-  unsigned char* stages = zr_raw + Z::kHead + NG * kGroup;
-  const int64_t ntiles = sv.ni * sv.n2;  // local z-lines
-  const int nc = int(sv.n3c);
-  const int ncr = (nc + 31) & ~31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < nstages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], GT / 32);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (int(threadIdx.x) >= NG * GT) {  // producer warp
-    if ((threadIdx.x & 31) == 0) {
-      Ring rg(nstages);
-      int k = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k, rg.next()) {
-        if (k >= nstages) mbar_wait(&empty[rg.s], rg.phase ^ 1u);
-        double* d = reinterpret_cast<double*>(stages + size_t(rg.s) * stage_bytes);
-        mbar_expect_tx(&full[rg.s], stage_bytes);
-#pragma unroll 1
-        for (int c = 0; c < 9; ++c) bulk_g2s(d + c * N, src + c * Nf + tile * N, uint32_t(N) * 8u, &full[rg.s]);
-      }
-    }
-    return;
-  }
-  const int g = int(threadIdx.x) / GT, tid = int(threadIdx.x) - g * GT;
-  const GroupSync gsync{1 + g, GT};
-  double2* work = reinterpret_cast<double2*>(zr_raw + Z::kHead + g * kGroup);
-  int64_t* zr = reinterpret_cast<int64_t*>(zr_raw + Z::kHead + g * kGroup + Z::kWork);
-  const int u = tid % TL, p = tid / TL;  // p < NP always (GT = NP * TL)
-  const int ca = 2 * p, cb = 2 * p + 1;
-  const bool hasb = cb < 9;
-  Ring rg(nstages);
-  int k = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k, rg.next()) {
-    if (k % NG != g) continue;
-    gsync();  // the previous tile's split has left the pair lines / row offsets
-    if (tid < 9) zr[tid] = sv.zrow(tid, tile);
-    mbar_wait(&full[rg.s], rg.phase);
-    const double* d = reinterpret_cast<const double*>(stages + size_t(rg.s) * stage_bytes);
-    double2 v[1][8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = rr_first_pos<L, false>(u, i);
-      v[0][i].x = d[ca * N + e];
-      v[0][i].y = hasb ? d[cb * N + e] : 0.0;
-    }
-    gsync();  // stage consumed
-    if ((tid & 31) == 0) mbar_arrive(&empty[rg.s]);
-    auto addr = [&](int, int pos) { return p * LS + pad8(pos); };
-    rr_stages<L, false, false, 0, 1>(v, u, true, work, tw, addr, gsync);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) work[p * LS + pad8(rr_final_pos<L, false>(u, i))] = v[0][i];
-    gsync();
-    for (int t = tid; t < NP * ncr; t += GT) {
-      const int pp = t / ncr, kk = t - pp * ncr;
-      if (kk >= nc) continue;
-      const double2 zk = work[pp * LS + pad8(kk)];
-      const double2 zm = work[pp * LS + pad8(kk == 0 ? 0 : N - kk)];
-      const int rl = 2 * pp;
-      sv.spec[zr[rl] + kk] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-      if (rl + 1 < 9) sv.spec[zr[rl + 1] + kk] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-    }
-  }
-}
-
 // ------------------------------------------------------------------ Y pass
 // W columns (lines) per block, thread -> (line = tid % W, u = tid / W)
 // one tile: columns [kc0, kc0 + W) of component c, local plane i

@@ -361,8 +361,15 @@ struct MatvecArgs {
   double step_prev;
   // bulk kernel only: per-tile sums of pdir . q (pdir^T A pdir; equals
   // pdir^T Pi(q) of solver.cpp:181 because pdir lies in the range of the
-  // self-adjoint projection Pi), one value per kMvT-cell tile; may be null
+  // self-adjoint projection Pi), one value per warp of each kMvT-cell tile
+  // ([tile][warp]); may be null
   double* pq_part;
+  // bulk kernel, RUPD variant: the residual update r -= rstep * ap of the
+  // previous CG iteration (solver.cpp:187) applied where r is read anyway;
+  // pq_part then holds two sums per warp, pdir . q and r . q
+  const double* ap;
+  double rstep;
+  double* r_out;  // = r (written in place)
 };
 
 __device__ __forceinline__ void mv_cell(const MatvecArgs& a, int64_t cell, double* y) {
@@ -423,7 +430,7 @@ static __global__ void __launch_bounds__(kEwThreads, MINB) k_matvec(MatvecArgs a
 // memory and store pdir, x and q. Cells past the last full tile are done by
 // block 0 with direct loads. Requires N even and 16-byte aligned rows.
 constexpr int kMvT = 256;
-constexpr int kMvHead = 256;  // barriers + reduction slots ahead of the ring
+constexpr int kMvHead = 128;  // barriers ahead of the ring
 
 template <bool FIRST, bool HASX>
 struct MvStage {
@@ -431,14 +438,14 @@ struct MvStage {
   static constexpr int kBytes = kRows * kMvT * 8 + kMvT * 4;
 };
 
-template <bool FIRST, bool HASX>
+template <bool FIRST, bool HASX, bool RUPD = false>
 static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs a, double* __restrict__ q,
                                                                       int nstages) {
-  using S = MvStage<FIRST, HASX>;
+  static_assert(!RUPD || (!FIRST && HASX), "the deferred residual update rides on later CG iterations");
+  using S = MvStage<FIRST, HASX>;  // RUPD: rows 27..35 carry ap, x is read directly
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + 8;
-  double* red = reinterpret_cast<double*>(smem_raw + 128);  // [2][8] warp sums of pdir . q
   unsigned char* buf = smem_raw + kMvHead;
   const int64_t N = a.N;
   const int64_t nfull = N / kMvT;
@@ -466,7 +473,7 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
           bulk_g2s(d + c * kMvT, a.r + c * N + off, rb, &full[rg.s]);
           bulk_g2s(d + (9 + c) * kMvT, a.fin + c * N + off, rb, &full[rg.s]);
           if (!FIRST) bulk_g2s(d + (18 + c) * kMvT, a.pdir + c * N + off, rb, &full[rg.s]);
-          if (!FIRST && HASX) bulk_g2s(d + (27 + c) * kMvT, a.xv + c * N + off, rb, &full[rg.s]);
+          if (!FIRST && HASX) bulk_g2s(d + (27 + c) * kMvT, (RUPD ? a.ap : a.xv) + c * N + off, rb, &full[rg.s]);
         }
         bulk_g2s(d + S::kRows * kMvT, a.cd.cid + off, kMvT * 4, &full[rg.s]);
       }
@@ -475,15 +482,37 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
   }
   const int tid = threadIdx.x;
   Ring rg(nstages);
-  int par = 0;
   for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x, rg.next()) {
+    const int64_t cell = t * kMvT + tid;
+    [[maybe_unused]] double xo[9], rn[9];
+    if constexpr (RUPD) {
+      // x comes straight from global memory (its ring rows carry ap); issued
+      // ahead of the stage wait
+#pragma unroll
+      for (int c = 0; c < 9; ++c) xo[c] = a.xv[c * N + cell];
+    }
     mbar_wait(&full[rg.s], rg.phase);
     const double* d = reinterpret_cast<const double*>(buf + size_t(rg.s) * S::kBytes);
-    const int64_t cell = t * kMvT + tid;
     double x[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) x[c] = d[c * kMvT + tid];
-    if (!FIRST) {
+    if constexpr (RUPD) {
+      // r <- r - rstep * ap (the update of k_cg_update), then
+      // x += step_prev * pdir_old
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        x[c] -= a.rstep * d[(27 + c) * kMvT + tid];
+        rn[c] = x[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 9; ++c) a.r_out[c * N + cell] = rn[c];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        const double po = d[(18 + c) * kMvT + tid];
+        a.xv[c * N + cell] = xo[c] + a.step_prev * po;
+        x[c] += a.beta * po;
+      }
+    } else if (!FIRST) {
 #pragma unroll
       for (int c = 0; c < 9; ++c) {
         const double po = d[(18 + c) * kMvT + tid];
@@ -514,21 +543,24 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
 #pragma unroll
     for (int c = 0; c < 9; ++c) q[c * N + cell] = y[c];
     if (a.pq_part) {
-      // fixed-order tile sum: 9 products per cell, warp tree, 8 warp sums
-      double dq = 0.0;
+      // fixed-order sums per warp of the tile (9 products per cell, warp
+      // tree); no block barrier: the consumer warps stay decoupled
+      constexpr int NQ = RUPD ? 2 : 1;
+      double dq[NQ];
+      dq[0] = 0.0;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) dq += x[c] * y[c];
+      for (int c = 0; c < 9; ++c) dq[0] += x[c] * y[c];
+      if constexpr (RUPD) {
+        dq[1] = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dq += __shfl_down_sync(0xffffffffu, dq, o);
-      if (lane == 0) red[par * 8 + warp] = dq;
-      asm volatile("bar.sync 1, %0;" ::"n"(kMvT) : "memory");
-      if (tid == 0) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < kMvT / 32; ++w) sum += red[par * 8 + w];
-        a.pq_part[t] = sum;
+        for (int c = 0; c < 9; ++c) dq[1] += rn[c] * y[c];
       }
-      par ^= 1;
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dq[i] += __shfl_down_sync(0xffffffffu, dq[i], o);
+        if (lane == 0) a.pq_part[(t * (kMvT / 32) + warp) * NQ + i] = dq[i];
+      }
     }
   }
   if (blockIdx.x == 0) {
@@ -713,6 +745,28 @@ static __global__ void k_reduce_partials(const double* __restrict__ partials, in
   if (threadIdx.x == 0) out[r] = sm[0];
 }
 
+// First level for long partial vectors: block b sums partials
+// [b chunk, (b + 1) chunk) of every value in a fixed order (strided
+// assignment + fixed tree) -> out[b][nred]; k_reduce_partials finishes.
+static __global__ void k_reduce_chunks(const double* __restrict__ partials, int64_t nblocks, int nred, int chunk,
+                                       double* __restrict__ out) {
+  __shared__ double sm[256];
+  const int64_t b0 = int64_t(blockIdx.x) * chunk;
+  const int64_t b1 = min(b0 + int64_t(chunk), nblocks);
+  for (int r = 0; r < nred; ++r) {
+    double s = 0.0;
+    for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) s += partials[b * nred + r];
+    sm[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x >> 1; w > 0; w >>= 1) {
+      if (int(threadIdx.x) < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[int64_t(blockIdx.x) * nred + r] = sm[0];
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------ FFT functors
 // FIELDS = real 9N-field streams (reads + writes) besides the spectrum; used
 // for the algorithmic-bytes bookkeeping of the profiler.
@@ -759,6 +813,31 @@ struct ConsStore9 {
   __device__ __forceinline__ void prefetch(int, int64_t, int64_t) const {}
   __device__ __forceinline__ double comp(int c, int64_t cell, double v, double*) const {
     dst[c * N + cell] = v;
+    return 0.0;
+  }
+};
+
+// CG with the residual norm by recurrence: ap = Pi(q), sum of ap^2 (the
+// products with pdir and r are taken in the matvec, see MatvecArgs)
+struct ConsStoreAA {
+  static constexpr int NRED = 1;
+  static constexpr int NSC = 1;
+  static constexpr bool PERCOMP = false;
+  static constexpr int FIELDS = 1;
+  static constexpr bool LOADS = false;
+  double* dst;
+  int64_t N;
+  __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+      dst[c * N + cell] = v[c];
+      acc[0] += v[c] * v[c];
+    }
+  }
+  __device__ __forceinline__ void prefetch(int, int64_t, int64_t) const {}
+  __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
+    dst[c * N + cell] = v;
+    sc[0] += v * v;
     return 0.0;
   }
 };

@@ -39,7 +39,9 @@ for name in a.cases:
     t_pre = time.perf_counter() - t0
     cm = CellMaterials(ctx, cfg.grid, kind, cp, nrm, neo_hookean(*cfg.matrix), neo_hookean(*cfg.inclusion))
     fbar, steps = case_fbar(cfg, case)
-    budget = case["max_ls"] if a.max_ls < 0 else a.max_ls
+    gold = os.path.join(ROOT, "tests", "golden", f"full_{name}.json")
+    doc = json.load(open(gold)) if os.path.exists(gold) else None
+    budget = (doc["max_ls"] if doc else case["max_ls"]) if a.max_ls < 0 else a.max_ls
     t1 = time.perf_counter()
     r = cm.solve(fbar, scheme=cfg.scheme, green=cfg.green, eval=cfg.eval, tol_equilibrium=cfg.tol,
                  max_outer=cfg.max_outer, load_steps=steps, max_ls_iterations=budget, want_fields=False)
@@ -52,4 +54,12 @@ for name in a.cases:
         print(f"  step {i}: newton {s['outer_iters']} cg {s['cg_iters']} cuts {s['line_search_cuts']} "
               f"ls r/c/t {s['ls_residual']}/{s['ls_cg']}/{s['ls_trial']} resid {s['residuals'][-1]:.3e} "
               f"sweep {s['sweep']}", flush=True)
+    if doc and budget == doc["max_ls"]:
+        # deviation of every recorded P-bar / residual from the oracle fixture
+        for i, (sa, sb) in enumerate(zip(rep["steps"], doc["report"]["steps"])):
+            dev = [float(np.linalg.norm(np.subtract(x, y)) / np.linalg.norm(y))
+                   for x, y in zip(sa["pbar_history"], sb["pbar_history"])]
+            rdev = [abs(x - y) / sb["residuals"][0] for x, y in zip(sa["residuals"], sb["residuals"])]
+            print(f"  step {i}: oracle newton {sb['outer_iters']} cg {sb['cg_iters']}; pbar history deviations "
+                  f"{['%.1e' % d for d in dev]}; residual deviations {['%.1e' % d for d in rdev]}", flush=True)
 ctx.close()
