@@ -247,7 +247,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
-  p->r_defer = knob("COMBO_RDEFER", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
   p->zring_pf = knob("COMBO_ZRING_PF", 0);
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
@@ -529,13 +528,13 @@ int ahead_blocks(const combo_ctx* c, K kernel, int threads, size_t smem) {
 
 // CG matvec: bulk-staged persistent kernel (one CTA per SM) when the rows
 // are 16-byte aligned, else one cell per thread with direct loads.
-template <bool FIRST, bool HASX, bool RUPD = false>
+template <bool FIRST, bool HASX>
 void launch_matvec_bulk(combo_ctx* c, const MatvecArgs& a, double* q) {
   using S = combo_dev::MvStage<FIRST, HASX>;
   constexpr int kMaxSmem = 227 * 1024;
   const int stages = std::min(4, (kMaxSmem - combo_dev::kMvHead) / S::kBytes);
   const size_t smem = combo_dev::kMvHead + size_t(stages) * S::kBytes;
-  auto kern = combo_dev::k_matvec_bulk<FIRST, HASX, RUPD>;
+  auto kern = combo_dev::k_matvec_bulk<FIRST, HASX>;
   static bool attr = false;  // per instantiation
   if (!attr) {
     COMBO_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -560,8 +559,6 @@ void launch_matvec(combo_ctx* c, const MatvecArgs& a, double* q) {
   }
   if (a.first)
     launch_matvec_bulk<true, false>(c, a, q);
-  else if (a.xv && a.ap)
-    launch_matvec_bulk<false, true, true>(c, a, q);
   else if (a.xv)
     launch_matvec_bulk<false, true>(c, a, q);
   else
@@ -1247,10 +1244,6 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
   // matvec and tiles that do not straddle planes (decomposition invariance).
   bool pq = !dfmg && c_->plan->pq_dot && !c_->plan->fuse_mv && (c_->dims[1] * c_->dims[2]) % combo_dev::kMvT == 0;
   const int64_t ntiles = (c_->N / combo_dev::kMvT) * (combo_dev::kMvT / 32);  // per-warp sums
-  // ... and the residual update deferred into the next matvec, r^T r by the
-  // recurrence rr' = rr - 2 s (r . q) + s^2 |ap|^2 (r . ap = r . q as above)
-  // whenever it loses at most 4 digits; else the direct update (k_cg_update)
-  double rstep = 0.0;
   while (it < cfg_.cg_max) {
     count_ls();
     ++rep.ls_cg;
@@ -1274,30 +1267,23 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
       } else {
         for (size_t k = 0; k < rk_.size(); ++k) {
           combo_ctx* m = rk_[k].c;
-          const bool rdef = pq && c_->plan->r_defer;
-          // + q write; deferred residual update: + ap read, r write
-          ProfScope ps(m, kTagMatvec, mvb + (rdef && it > 0 ? 216.0 : 72.0) * double(rk_[k].N));
+          ProfScope ps(m, kTagMatvec, mvb + 72.0 * double(rk_[k].N));
           MatvecArgs a = mv(k).a;
-          if (pq) a.pq_part = part_ptr(m, ntiles, rdef && it > 0 ? 2 : 1);
-          if (rdef && it > 0) {
-            a.ap = P(ap_, k);
-            a.rstep = rstep;
-            a.r_out = P(r_, k);
-          }
+          if (pq) a.pq_part = part_ptr(m, ntiles, 1);
           launch_matvec(m, a, P(rb_, k));
           ++m->launches;
           COMBO_CK(cudaGetLastError());
         }
-        if (pq && c_->plan->r_defer) {
-          group_reduce(c_, ntiles, it > 0 ? 2 : 1, 20);  // pdir . q (, r . q) -> 20 (, 21)
-          project_group(
-              c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
-              [&](size_t k) { return ConsStoreAA{P(ap_, k), rk_[k].N}; }, 22);  // |ap|^2 -> 22
-        } else if (pq) {
+        if (pq) {
+          // pap -> dres[20], s = rr / pap -> dres[24]; the z-inverse updates r and sums r^T r -> dres[21]
           group_reduce(c_, ntiles, 1, 20);
+          combo_ctx* L = c_;
+          k_cg_step<<<1, 1, 0, L->stream>>>(L->dres.p + 20, rr, L->dres.p + 24);
+          ++L->launches;
+          COMBO_CK(cudaGetLastError());
           project_group(
               c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
-              [&](size_t k) { return ConsStore9{P(ap_, k), rk_[k].N}; }, 20);
+              [&](size_t k) { return ConsCgUpdate{P(r_, k), L->dres.p + 24, rk_[k].N}; }, 21);
         } else {
           project_group(
               c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; }, cons, 20);
@@ -1314,34 +1300,18 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
     }
     const double step = rr / pap;
     if (dfmg) axpy_x(step);
-    if (pq && c_->plan->r_defer) {
-      // first iteration: pdir = r, so r . q = pdir . q
-      const double rq = it > 0 ? c_->hres[21] : pap;
-      const double rr_rec = rr - 2.0 * step * rq + step * step * c_->hres[22];
-      if (rr_rec >= 1e-4 * rr) {
-        rstep = step;
-        ++it;
-        step_prev = step;
-        if (std::sqrt(rr_rec) <= tol_rel * bnorm) {
-          flush_x();
-          return it;
-        }
-        beta = rr_rec / rr;
-        rr = rr_rec;
-        continue;
+    if (!pq) {
+      for (auto& r : rk_) {
+        double* part = part_ptr(r.c, nbc, 1);
+        ProfScope ps(r.c, kTagCgUpdate, 216.0 * double(r.N));
+        k_cg_update<<<unsigned(nbc), kEwThreads, 0, r.c->stream>>>(r.f[r_].p, r.f[ap_].p, step, r.N, chunks_of(r.c),
+                                                                     part);
+        ++r.c->launches;
+        COMBO_CK(cudaGetLastError());
       }
-      rstep = 0.0;  // strong cancellation: update r and take its norm directly below
+      group_reduce(c_, nbc, 1, 21);
+      fetch_results(c_, false);
     }
-    for (auto& r : rk_) {
-      double* part = part_ptr(r.c, nbc, 1);
-      ProfScope ps(r.c, kTagCgUpdate, 216.0 * double(r.N));
-      k_cg_update<<<unsigned(nbc), kEwThreads, 0, r.c->stream>>>(r.f[r_].p, r.f[ap_].p, step, r.N, chunks_of(r.c),
-                                                                   part);
-      ++r.c->launches;
-      COMBO_CK(cudaGetLastError());
-    }
-    group_reduce(c_, nbc, 1, 21);
-    fetch_results(c_, false);
     ++it;
     step_prev = step;
     const double rr_new = c_->hres[21];

@@ -364,12 +364,6 @@ struct MatvecArgs {
   // self-adjoint projection Pi), one value per warp of each kMvT-cell tile
   // ([tile][warp]); may be null
   double* pq_part;
-  // bulk kernel, RUPD variant: the residual update r -= rstep * ap of the
-  // previous CG iteration (solver.cpp:187) applied where r is read anyway;
-  // pq_part then holds two sums per warp, pdir . q and r . q
-  const double* ap;
-  double rstep;
-  double* r_out;  // = r (written in place)
 };
 
 __device__ __forceinline__ void mv_cell(const MatvecArgs& a, int64_t cell, double* y) {
@@ -438,11 +432,10 @@ struct MvStage {
   static constexpr int kBytes = kRows * kMvT * 8 + kMvT * 4;
 };
 
-template <bool FIRST, bool HASX, bool RUPD = false>
+template <bool FIRST, bool HASX>
 static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs a, double* __restrict__ q,
                                                                       int nstages) {
-  static_assert(!RUPD || (!FIRST && HASX), "the deferred residual update rides on later CG iterations");
-  using S = MvStage<FIRST, HASX>;  // RUPD: rows 27..35 carry ap, x is read directly
+  using S = MvStage<FIRST, HASX>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + 8;
@@ -473,7 +466,7 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
           bulk_g2s(d + c * kMvT, a.r + c * N + off, rb, &full[rg.s]);
           bulk_g2s(d + (9 + c) * kMvT, a.fin + c * N + off, rb, &full[rg.s]);
           if (!FIRST) bulk_g2s(d + (18 + c) * kMvT, a.pdir + c * N + off, rb, &full[rg.s]);
-          if (!FIRST && HASX) bulk_g2s(d + (27 + c) * kMvT, (RUPD ? a.ap : a.xv) + c * N + off, rb, &full[rg.s]);
+          if (!FIRST && HASX) bulk_g2s(d + (27 + c) * kMvT, a.xv + c * N + off, rb, &full[rg.s]);
         }
         bulk_g2s(d + S::kRows * kMvT, a.cd.cid + off, kMvT * 4, &full[rg.s]);
       }
@@ -483,36 +476,13 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
   const int tid = threadIdx.x;
   Ring rg(nstages);
   for (int64_t t = blockIdx.x; t < nfull; t += gridDim.x, rg.next()) {
-    const int64_t cell = t * kMvT + tid;
-    [[maybe_unused]] double xo[9], rn[9];
-    if constexpr (RUPD) {
-      // x comes straight from global memory (its ring rows carry ap); issued
-      // ahead of the stage wait
-#pragma unroll
-      for (int c = 0; c < 9; ++c) xo[c] = a.xv[c * N + cell];
-    }
     mbar_wait(&full[rg.s], rg.phase);
     const double* d = reinterpret_cast<const double*>(buf + size_t(rg.s) * S::kBytes);
+    const int64_t cell = t * kMvT + tid;
     double x[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) x[c] = d[c * kMvT + tid];
-    if constexpr (RUPD) {
-      // r <- r - rstep * ap (the update of k_cg_update), then
-      // x += step_prev * pdir_old
-#pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        x[c] -= a.rstep * d[(27 + c) * kMvT + tid];
-        rn[c] = x[c];
-      }
-#pragma unroll
-      for (int c = 0; c < 9; ++c) a.r_out[c * N + cell] = rn[c];
-#pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        const double po = d[(18 + c) * kMvT + tid];
-        a.xv[c * N + cell] = xo[c] + a.step_prev * po;
-        x[c] += a.beta * po;
-      }
-    } else if (!FIRST) {
+    if (!FIRST) {
 #pragma unroll
       for (int c = 0; c < 9; ++c) {
         const double po = d[(18 + c) * kMvT + tid];
@@ -543,24 +513,14 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
 #pragma unroll
     for (int c = 0; c < 9; ++c) q[c * N + cell] = y[c];
     if (a.pq_part) {
-      // fixed-order sums per warp of the tile (9 products per cell, warp
+      // fixed-order sum per warp of the tile (9 products per cell, warp
       // tree); no block barrier: the consumer warps stay decoupled
-      constexpr int NQ = RUPD ? 2 : 1;
-      double dq[NQ];
-      dq[0] = 0.0;
+      double dq = 0.0;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) dq[0] += x[c] * y[c];
-      if constexpr (RUPD) {
-        dq[1] = 0.0;
+      for (int c = 0; c < 9; ++c) dq += x[c] * y[c];
 #pragma unroll
-        for (int c = 0; c < 9; ++c) dq[1] += rn[c] * y[c];
-      }
-#pragma unroll
-      for (int i = 0; i < NQ; ++i) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dq[i] += __shfl_down_sync(0xffffffffu, dq[i], o);
-        if (lane == 0) a.pq_part[(t * (kMvT / 32) + warp) * NQ + i] = dq[i];
-      }
+      for (int o = 16; o > 0; o >>= 1) dq += __shfl_down_sync(0xffffffffu, dq, o);
+      if (lane == 0) a.pq_part[t * (kMvT / 32) + warp] = dq;
     }
   }
   if (blockIdx.x == 0) {
@@ -817,30 +777,46 @@ struct ConsStore9 {
   }
 };
 
-// CG with the residual norm by recurrence: ap = Pi(q), sum of ap^2 (the
-// products with pdir and r are taken in the matvec, see MatvecArgs)
-struct ConsStoreAA {
+// CG with the step length known before the projection (pdir^T A pdir comes
+// from the matvec, MatvecArgs::pq_part): the z-inverse applies
+// r -= s Pi(q) itself and sums r^T r (solver.cpp:186-190), so ap = Pi(q) is
+// never stored and k_cg_update's pass over r and ap disappears.
+// s = rr / pap is formed on the device (k_cg_step) from the reduced pap.
+struct ConsCgUpdate {
   static constexpr int NRED = 1;
   static constexpr int NSC = 1;
   static constexpr bool PERCOMP = false;
-  static constexpr int FIELDS = 1;
-  static constexpr bool LOADS = false;
-  double* dst;
+  static constexpr int FIELDS = 2;
+  static constexpr bool LOADS = true;
+  double* r;
+  const double* step;  // device scalar
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
+    const double s = __ldg(step);
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
-      dst[c * N + cell] = v[c];
-      acc[0] += v[c] * v[c];
+      const double rn = r[c * N + cell] - s * v[c];
+      r[c * N + cell] = rn;
+      acc[0] += rn * rn;
     }
   }
-  __device__ __forceinline__ void prefetch(int, int64_t, int64_t) const {}
+  __device__ __forceinline__ void prefetch(int c, int64_t cell0, int64_t n) const {
+    bulk_prefetch_l2(r + c * N + cell0, size_t(n) * 8);
+  }
   __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
-    dst[c * N + cell] = v;
-    sc[0] += v * v;
+    const double rn = r[c * N + cell] - __ldg(step) * v;
+    r[c * N + cell] = rn;
+    sc[0] += rn * rn;
     return 0.0;
   }
 };
+
+// s = rr / pap (solver.cpp:186) on the device; pap <= 0 (CG breakdown,
+// detected by the host after the projection) leaves s = 0
+static __global__ void k_cg_step(const double* __restrict__ pap, double rr, double* __restrict__ step) {
+  const double p = *pap;
+  *step = p > 0.0 ? rr / p : 0.0;
+}
 
 // run_basic F update (solver.cpp:135-149): F_new = fbar - Pi(tau)/alpha,
 // diff against the pinned F_old; sums of diff^2 and of F_new.

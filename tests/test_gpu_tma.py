@@ -127,14 +127,13 @@ def test_zinv_ring_solve_bitwise(oracle, scheme, green):
 
 
 def test_cg_sums_from_matvec_match_reference_cg(oracle):
-    """CG scalars taken where the operands already stream: pdir . q and r . q
-    summed in the matvec (pdir and r lie in the range of the self-adjoint
-    projection, so pdir . q = pdir . Pi(q), solver.cpp:180-181), the residual
-    update deferred into the next matvec and r^T r by the recurrence
-    rr - 2 s r.q + s^2 |ap|^2 (solver.cpp:186-190) -- against the dot
-    products taken after the projection / the direct update: same iteration
-    counts, P-bar and F equal to rounding; P-bar within 1e-9 and F within
-    1e-7 of the oracle."""
+    """CG with pdir^T A pdir summed in the matvec as pdir . q (pdir lies in
+    the range of the self-adjoint projection, so pdir . q = pdir . Pi(q),
+    solver.cpp:180-181) and the residual update r -= s Pi(q) + r^T r done by
+    the z-inverse itself (solver.cpp:186-190; ap is never stored) -- against
+    the dot product after the projection and the separate update pass: same
+    iteration counts, P-bar and F equal to rounding; P-bar within 1e-9 and F
+    within 1e-7 of the oracle."""
     import paper_2204_13624_b200 as pkg
 
     fine, fac = (64, 64, 64), (2, 2, 2)
@@ -143,7 +142,7 @@ def test_cg_sums_from_matvec_match_reference_cg(oracle):
     fbar[0, 0] += 0.05
     fbar[1, 2] += 0.03
     runs = []
-    for knobs in (dict(COMBO_PQ=1, COMBO_RDEFER=1), dict(COMBO_PQ=1, COMBO_RDEFER=0), dict(COMBO_PQ=0)):
+    for knobs in (dict(COMBO_PQ=1), dict(COMBO_PQ=0)):
         c, old = _fresh_ctx(**knobs)
         try:
             img = c.generate("rsa_spheres", fine, (1, 1, 1), 5, 4.0, 8.0, 0.3)
@@ -157,8 +156,7 @@ def test_cg_sums_from_matvec_match_reference_cg(oracle):
             _restore(old)
             c.close()
     (a, prof, grid) = runs[0]
-    assert "cg_update" not in prof or prof["cg_update"]["launches"] < prof["matvec"]["launches"] // 4
-    assert "cg_update" in runs[1][1]
+    assert "cg_update" not in prof and "cg_update" in runs[1][1]
     for b, _, _ in runs[1:]:
         assert a["report"]["success"] and b["report"]["success"]
         for sa, sb in zip(a["report"]["steps"], b["report"]["steps"]):

@@ -1,6 +1,6 @@
 # one ncu --set full capture of the LS kernels of a bounded solve (tools/prof_ls.py)
 # usage: bash tools/ncu_ls.sh <tag> [kernel regex] [count]
-tag=${1:-x}; rx=${2:-"k_matvec|zfwd_rr|ypass_rr|xgamma|zinv_rr|k_cg_update|k_sweep|k_comp_tangent"}; cnt=${3:-16}
+tag=${1:-x}; rx=${2:-"k_matvec|zfwd|ypass|xgamma|zinv|k_cg_update|k_sweep|k_comp_tangent"}; cnt=${3:-20}
 mkdir -p gpurun_out
 python tools/prof_ls.py --ls 4 > gpurun_out/plain_ls_$tag.log 2>&1 || exit 1
 ncu --set full --clock-control none --import-source on -k "regex:$rx" -c $cnt \

@@ -16,7 +16,7 @@ python tools/launch_summary.py /tmp/launches_$tag.csv > $out/launches_$tag.txt
 gzip -c /tmp/launches_$tag.csv > $out/launches_$tag.csv.gz
 python tools/prof_ls.py --ls 4 > $out/plain_ls_$tag.log 2>&1
 ncu --set full --clock-control none --import-source on \
-  -k "regex:k_matvec|zfwd_rr|ypass_rr|xgamma|zinv_rr|k_cg_update|k_sweep|k_comp_tangent" -c 16 \
+  -k "regex:k_matvec|zfwd|ypass|xgamma|zinv|k_cg_update|k_sweep|k_comp_tangent" -c 20 \
   -o /tmp/ls_$tag python tools/prof_ls.py --ls 4 > /tmp/ncu_ls_$tag.log 2>&1
 python tools/ncu_summary.py /tmp/ls_$tag.ncu-rep > $out/ncu_full_$tag.txt
 ncu -i /tmp/ls_$tag.ncu-rep --page raw --csv > /tmp/raw_$tag.csv
