@@ -103,13 +103,12 @@ struct FftPlan {
   size_t zsmem = 0, ysmem = 0, xsmem = 0;
   // register-resident pow2 path (fft_rr.cuh), used when the axis length is
   // a power of two >= 8
-  int rzL = 1, rzT = 32, rzLc = 1, rzTc = 32, ryW = 8, ryT = 32, rxW = 4, rxT = 32;
+  int rzL = 1, rzT = 32, ryW = 8, ryT = 32, rxW = 4, rxT = 32;
   size_t rzsmem = 0, rysmem = 0, rxsmem = 0;
   int xminb = 2;  // xgamma_v4 blocks per SM (launch bound)
   bool split_sweep = true;  // composite Newton pass + pure streaming pass (COMBO_SPLIT_SWEEP=0: one pass)
   bool mv_bulk = true;  // bulk-staged CG matvec (COMBO_MV_BULK=0: one cell per thread, direct loads)
   bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
-  bool fuse_mv = false;  // CG matvec fused into the Z-forward pass (COMBO_FUSE_MV=1)
   bool pq_dot = true;    // CG: pdir^T A pdir summed in the matvec (COMBO_PQ=0: in the z-inverse consumer)
   // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
   // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off

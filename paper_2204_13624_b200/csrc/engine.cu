@@ -244,7 +244,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     return v ? std::atoi(v) : dflt;
   };
   p->xminb = knob("COMBO_XMINB", 2);
-  p->fuse_mv = knob("COMBO_FUSE_MV", 0) != 0;
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
@@ -265,9 +264,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     p->rzL = int(Lz);
     const int64_t np = (9 * Lz + 1) / 2;
     p->rzT = int((np * tl + 31) / 32 * 32);
-    // fused matvec producer: <= 384 threads (register budget of the NH code)
-    p->rzLc = int(divisor_le(lines_for(384)));
-    p->rzTc = int((((9 * p->rzLc + 1) / 2) * tl + 31) / 32 * 32);
     p->rzsmem = size_t(np * (n3 + n3 / 8)) * sizeof(double2);
   }
   // j-major rows (single slab): x+Gamma 5.9 ms, y 4.05 / 4.09 ms; i-major: 6.8, 4.01 / 4.03 (512^3, round 1)
@@ -569,15 +565,15 @@ template <class Prod>
 int64_t launch_zfwd(combo_ctx* c, const Prod& prod, double extra_bytes = 0.0) {
   FftPlan& p = *c->plan;
   int64_t nb = 0;
-  ProfScope ps(c, Prod::CELL ? kTagMvZfwd : kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
+  ProfScope ps(c, kTagZfwd, spec_bytes(c) + 72.0 * double(c->N) * Prod::FIELDS + extra_bytes);
   dispatch_log2(p.dims[2], [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     if constexpr (L >= 3) {
-      const int lz = Prod::CELL ? p.rzLc : p.rzL;
+      const int lz = p.rzL;
       nb = (p.ni * p.dims[1] + lz - 1) / lz;
       auto k = zfwd_rr<Prod, L>;
       smem_attr(k, p.rzsmem);
-      k<<<unsigned(nb), Prod::CELL ? p.rzTc : p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, lz, prod,
+      k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, lz, prod,
                                                                           nullptr);
     } else {
       nb = (p.ni * p.dims[1] + p.zL - 1) / p.zL;
@@ -1240,9 +1236,10 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
   };
   auto cons = [&](size_t k) { return ConsCg{P(ap_, k), P(pd_, k), rk_[k].N}; };
   // pdir^T A pdir taken in the matvec as pdir . q (see MatvecArgs::pq_part):
-  // the z-inverse then only stores ap and never reads pdir. Needs the bulk
-  // matvec and tiles that do not straddle planes (decomposition invariance).
-  bool pq = !dfmg && c_->plan->pq_dot && !c_->plan->fuse_mv && (c_->dims[1] * c_->dims[2]) % combo_dev::kMvT == 0;
+  // the step is known before the projection, whose z-inverse applies
+  // r -= s Pi(q) and sums r^T r (ConsCgUpdate). Needs the bulk matvec and
+  // tiles that do not straddle planes (decomposition invariance).
+  bool pq = !dfmg && c_->plan->pq_dot && (c_->dims[1] * c_->dims[2]) % combo_dev::kMvT == 0;
   const int64_t ntiles = (c_->N / combo_dev::kMvT) * (combo_dev::kMvT / 32);  // per-warp sums
   while (it < cfg_.cg_max) {
     count_ls();
@@ -1256,34 +1253,38 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
       // r, F, cid, pdir (r/w), x (r/w, deferred update); composite packed tangents
       auto mv = [&](size_t k) {
         combo_ctx* m = rk_[k].c;
-        return ProdMatvec{{m->mp, m->cell_data(), P(F_, k), shF_, P(r_, k), P(pd_, k), beta, it == 0 ? 1 : 0,
-                           rk_[k].N, P(x_, k), step_prev, nullptr}};
+        return MatvecArgs{m->mp, m->cell_data(), P(F_, k), shF_, P(r_, k), P(pd_, k), beta, it == 0 ? 1 : 0,
+                          rk_[k].N, P(x_, k), step_prev, nullptr};
       };
       if (pq)
-        for (size_t k = 0; k < rk_.size(); ++k) pq = pq && mv_bulk_ok(rk_[k].c, mv(k).a);
+        for (size_t k = 0; k < rk_.size(); ++k) pq = pq && mv_bulk_ok(rk_[k].c, mv(k));
       const double mvb = (it == 0 ? 220.0 : 436.0) * double(c_->N) + 360.0 * double(c_->ncomp);
-      if (c_->plan->fuse_mv) {
-        project_group(c_, cfg_.green, mv, cons, 20, mvb);
-      } else {
+      {
         for (size_t k = 0; k < rk_.size(); ++k) {
           combo_ctx* m = rk_[k].c;
           ProfScope ps(m, kTagMatvec, mvb + 72.0 * double(rk_[k].N));
-          MatvecArgs a = mv(k).a;
+          MatvecArgs a = mv(k);
           if (pq) a.pq_part = part_ptr(m, ntiles, 1);
           launch_matvec(m, a, P(rb_, k));
           ++m->launches;
           COMBO_CK(cudaGetLastError());
         }
         if (pq) {
-          // pap -> dres[20], s = rr / pap -> dres[24]; the z-inverse updates r and sums r^T r -> dres[21]
+          // pap -> dres[20]; the host forms s = rr / pap (one scalar round
+          // trip), the z-inverse writes r' = r - s Pi(q) into the free ap
+          // slot and sums r'^T r' -> dres[21]
           group_reduce(c_, ntiles, 1, 20);
-          combo_ctx* L = c_;
-          k_cg_step<<<1, 1, 0, L->stream>>>(L->dres.p + 20, rr, L->dres.p + 24);
-          ++L->launches;
-          COMBO_CK(cudaGetLastError());
+          fetch_results(c_, false);
+          const double pap = c_->hres[20];
+          if (!(pap > 0.0)) {
+            breakdown = true;  // solver.cpp:182-185 (see below)
+            return it;
+          }
+          const double s = rr / pap;
           project_group(
               c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
-              [&](size_t k) { return ConsCgUpdate{P(r_, k), L->dres.p + 24, rk_[k].N}; }, 21);
+              [&](size_t k) { return ConsCgUpdate{P(r_, k), P(ap_, k), s, rk_[k].N}; }, 21);
+          std::swap(r_, ap_);
         } else {
           project_group(
               c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; }, cons, 20);

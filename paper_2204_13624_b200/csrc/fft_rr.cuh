@@ -264,29 +264,7 @@ __device__ __forceinline__ void zfwd_tile(const SpecView& sv, const double2* __r
   const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
   const bool hasb = rlb < nreal;
   double2 v[1][8];
-  if constexpr (Prod::CELL) {
-    // per-cell producer: all 9 components of the block's cells into the
-    // pair lines in shared memory, then the first stage reads from there
-    double* smd = reinterpret_cast<double*>(sm);
-    for (int t = threadIdx.x; t < nlines * N; t += blockDim.x) {
-      const int l = t >> L, k = t & (N - 1);
-      double y[9];
-      prod(line0 * N + t, y, nullptr);
-#pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        const int rl = 9 * l + c;
-        smd[2 * ((rl >> 1) * LS + pad8(k)) + (rl & 1)] = y[c];
-      }
-    }
-    if (nreal & 1)
-      for (int k = threadIdx.x; k < N; k += blockDim.x) smd[2 * ((npair - 1) * LS + pad8(k)) + 1] = 0.0;
-    __syncthreads();
-    if (active) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[0][i] = sm[p * LS + pad8(rr_first_pos<L, false>(u, i))];
-    }
-    __syncthreads();
-  } else if (active) {
+  if (active) {
     const int64_t cella = (line0 + la) * N, cellb = (line0 + lb) * N;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -323,7 +301,7 @@ __device__ __forceinline__ void zfwd_tile(const SpecView& sv, const double2* __r
 }
 
 template <class Prod, int L>
-static __global__ void __launch_bounds__(Prod::CELL ? 384 : 512, 2)
+static __global__ void __launch_bounds__(512, 2)
     zfwd_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, Prod prod, double*) {
   const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;

@@ -736,7 +736,6 @@ static __global__ void k_reduce_chunks(const double* __restrict__ partials, int6
 struct ProdLoad9 {
   static constexpr int NRED = 0;
   static constexpr int FIELDS = 1;
-  static constexpr bool CELL = false;  // comp() interface
   const double* src;
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, double* v, double*) const {
@@ -744,18 +743,6 @@ struct ProdLoad9 {
     for (int c = 0; c < 9; ++c) v[c] = src[c * N + cell];
   }
   __device__ __forceinline__ double comp(int c, int64_t cell) const { return src[c * N + cell]; }
-};
-
-// CG matvec fused into the Z-forward pass (solver.cpp:194-197): the block
-// evaluates y = A : pdir for the cells of its z-lines into shared memory and
-// transforms them directly, so q never touches HBM. CELL producers use the
-// per-cell operator() on every path.
-struct ProdMatvec {
-  static constexpr int NRED = 0;
-  static constexpr int FIELDS = 0;  // bytes passed by the caller (first / later iterations differ)
-  static constexpr bool CELL = true;
-  MatvecArgs a;
-  __device__ __forceinline__ void operator()(int64_t cell, double* v, double*) const { mv_cell(a, cell, v); }
 };
 
 struct ConsStore9 {
@@ -779,24 +766,24 @@ struct ConsStore9 {
 
 // CG with the step length known before the projection (pdir^T A pdir comes
 // from the matvec, MatvecArgs::pq_part): the z-inverse applies
-// r -= s Pi(q) itself and sums r^T r (solver.cpp:186-190), so ap = Pi(q) is
-// never stored and k_cg_update's pass over r and ap disappears.
-// s = rr / pap is formed on the device (k_cg_step) from the reduced pap.
+// r' = r - s Pi(q) itself and sums r'^T r' (solver.cpp:186-190), so
+// ap = Pi(q) is never stored and k_cg_update's pass over r and ap
+// disappears. r' goes to a second field (the host swaps the slots).
 struct ConsCgUpdate {
   static constexpr int NRED = 1;
   static constexpr int NSC = 1;
   static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 2;
   static constexpr bool LOADS = true;
-  double* r;
-  const double* step;  // device scalar
+  const double* r;
+  double* rnew;
+  double step;
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
-    const double s = __ldg(step);
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
-      const double rn = r[c * N + cell] - s * v[c];
-      r[c * N + cell] = rn;
+      const double rn = r[c * N + cell] - step * v[c];
+      rnew[c * N + cell] = rn;
       acc[0] += rn * rn;
     }
   }
@@ -804,19 +791,12 @@ struct ConsCgUpdate {
     bulk_prefetch_l2(r + c * N + cell0, size_t(n) * 8);
   }
   __device__ __forceinline__ double comp(int c, int64_t cell, double v, double* sc) const {
-    const double rn = r[c * N + cell] - __ldg(step) * v;
-    r[c * N + cell] = rn;
+    const double rn = r[c * N + cell] - step * v;
+    rnew[c * N + cell] = rn;
     sc[0] += rn * rn;
     return 0.0;
   }
 };
-
-// s = rr / pap (solver.cpp:186) on the device; pap <= 0 (CG breakdown,
-// detected by the host after the projection) leaves s = 0
-static __global__ void k_cg_step(const double* __restrict__ pap, double rr, double* __restrict__ step) {
-  const double p = *pap;
-  *step = p > 0.0 ? rr / p : 0.0;
-}
 
 // run_basic F update (solver.cpp:135-149): F_new = fbar - Pi(tau)/alpha,
 // diff against the pinned F_old; sums of diff^2 and of F_new.

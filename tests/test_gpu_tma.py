@@ -156,7 +156,8 @@ def test_cg_sums_from_matvec_match_reference_cg(oracle):
             _restore(old)
             c.close()
     (a, prof, grid) = runs[0]
-    assert "cg_update" not in prof and "cg_update" in runs[1][1]
+    # only the x flush at the end of every CG solve keeps the cg_update tag
+    assert 4 * prof["cg_update"]["launches"] < runs[1][1]["cg_update"]["launches"]
     for b, _, _ in runs[1:]:
         assert a["report"]["success"] and b["report"]["success"]
         for sa, sb in zip(a["report"]["steps"], b["report"]["steps"]):
