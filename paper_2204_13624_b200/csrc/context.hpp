@@ -115,7 +115,8 @@ struct FftPlan {
   bool zbulk = false;  // z-inverse with spectrum rows staged per block (COMBO_ZBULK=1; measured slower: 2 blocks/SM)
   // persistent ring-staged z-inverse at n3 = 512 (two consumer groups; COMBO_ZRING=0: one block per
   // tile), used for consumers whose epilogue reads no field (Cons::LOADS)
-  int zring = 2, zring_pf = 0;
+  int zring = 2, zring_pf = 1;
+  bool zring_pre = true;  // ... or preloads them ahead of the stages (Cons::PRELOAD; COMBO_ZRING_PRE=0: one block per tile)
   bool tma_x = false, tma_y = false;
   int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
   CUtensorMap xmap{}, ymap{};

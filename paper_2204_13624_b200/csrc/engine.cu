@@ -247,7 +247,8 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
-  p->zring_pf = knob("COMBO_ZRING_PF", 0);
+  p->zring_pf = knob("COMBO_ZRING_PF", 1);
+  p->zring_pre = knob("COMBO_ZRING_PRE", 1) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -615,7 +616,7 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
           k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, scale, cons, part, stages, p.zring_pf);
           ring = true;
         };
-        if (p.zring >= 2 && p.rzL == 1 && !Cons::LOADS) go(std::integral_constant<int, 2>{});
+        if (p.zring >= 2 && p.rzL == 1 && (!Cons::LOADS || (Cons::PRELOAD && p.zring_pre))) go(std::integral_constant<int, 2>{});
       }
       if (ring) {
       } else if (p.zbulk && p.rzsmem % 128 == 0 && p.rzsmem + rows <= 100 * 1024) {

@@ -318,28 +318,47 @@ __device__ __forceinline__ void zinv_finish(double2* sm, const double2* __restri
   constexpr int N = 1 << L, TL = N / 8, LS = N + N / 8;
   const int u = tid % TL, p = tid / TL;
   const bool active = p < npair;
+  const int rla = 2 * p, rlb = 2 * p + 1;
+  const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
+  const bool hasb = rlb < nreal;
+  const int64_t cella = (line0 + la) * N, cellb = (line0 + lb) * N;
   double2 v[1][8];
   if (active) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[0][i] = sm[p * LS + pad8(rr_first_pos<L, false>(u, i))];
   }
+  // PRELOAD consumers: the field values the epilogue combines with the
+  // outputs are requested now, so their latency hides behind the stages
+  // (registers or, under pressure, L1-resident local memory)
+  [[maybe_unused]] double pre[2][8];
+  if constexpr (Cons::PRELOAD) {
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = rr_final_pos<L, false>(u, i);
+        pre[0][i] = cons.load(ca, cella + e);
+        pre[1][i] = hasb ? cons.load(cb, cellb + e) : 0.0;
+      }
+    }
+  }
   sync();
   auto addr = [&](int, int pos) { return p * LS + pad8(pos); };
   rr_stages<L, true, false, 0, 1>(v, u, active, sm, tw, addr, sync);
-  const int rla = 2 * p, rlb = 2 * p + 1;
-  const int la = rla / 9, ca = rla - 9 * la, lb = rlb / 9, cb = rlb - 9 * lb;
-  const bool hasb = rlb < nreal;
   double sc[Cons::NSC > 0 ? Cons::NSC : 1];
 #pragma unroll
   for (int i = 0; i < (Cons::NSC > 0 ? Cons::NSC : 1); ++i) sc[i] = 0.0;
   double pa = 0.0, pb = 0.0;
   if (active) {
-    const int64_t cella = (line0 + la) * N, cellb = (line0 + lb) * N;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int e = rr_final_pos<L, false>(u, i);
-      pa += cons.comp(ca, cella + e, v[0][i].x * scale, sc);
-      if (hasb) pb += cons.comp(cb, cellb + e, v[0][i].y * scale, sc);
+      if constexpr (Cons::PRELOAD) {
+        pa += cons.comp_pre(ca, cella + e, v[0][i].x * scale, pre[0][i], sc);
+        if (hasb) pb += cons.comp_pre(cb, cellb + e, v[0][i].y * scale, pre[1][i], sc);
+      } else {
+        pa += cons.comp(ca, cella + e, v[0][i].x * scale, sc);
+        if (hasb) pb += cons.comp(cb, cellb + e, v[0][i].y * scale, sc);
+      }
     }
   }
   if constexpr (Cons::NSC > 0 || Cons::PERCOMP) {

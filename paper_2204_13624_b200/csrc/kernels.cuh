@@ -751,6 +751,7 @@ struct ConsStore9 {
   static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 1;
   static constexpr bool LOADS = false;  // the epilogue reads fields (ring kernel: latency exposed)
+  static constexpr bool PRELOAD = false;  // fields requested ahead of the inverse stages (zinv_finish)
   double* dst;
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, const double* v, double*) const {
@@ -775,10 +776,18 @@ struct ConsCgUpdate {
   static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 2;
   static constexpr bool LOADS = true;
+  static constexpr bool PRELOAD = true;
   const double* r;
   double* rnew;
   double step;
   int64_t N;
+  __device__ __forceinline__ double load(int c, int64_t cell) const { return r[c * N + cell]; }
+  __device__ __forceinline__ double comp_pre(int c, int64_t cell, double v, double rold, double* sc) const {
+    const double rn = rold - step * v;
+    rnew[c * N + cell] = rn;
+    sc[0] += rn * rn;
+    return 0.0;
+  }
   __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
@@ -804,6 +813,7 @@ struct ConsBasic {
   static constexpr int NRED = 10;
   static constexpr int FIELDS = 2;
   static constexpr bool LOADS = true;  // the epilogue reads fields (ring kernel: latency exposed)
+  static constexpr bool PRELOAD = false;  // fields requested ahead of the inverse stages (zinv_finish)
   const double* fold;
   Shift9 fold_shift;
   double* fnew;
@@ -842,6 +852,7 @@ struct ConsResid {
   static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 1;
   static constexpr bool LOADS = false;  // the epilogue reads fields (ring kernel: latency exposed)
+  static constexpr bool PRELOAD = false;  // fields requested ahead of the inverse stages (zinv_finish)
   double* r;
   int64_t N;
   __device__ __forceinline__ void operator()(int64_t cell, const double* v, double* acc) const {
@@ -866,6 +877,7 @@ struct ConsCg {
   static constexpr bool PERCOMP = false;
   static constexpr int FIELDS = 2;
   static constexpr bool LOADS = true;  // the epilogue reads fields (ring kernel: latency exposed)
+  static constexpr bool PRELOAD = false;  // fields requested ahead of the inverse stages (zinv_finish)
   double* ap;
   const double* pdir;
   int64_t N;
