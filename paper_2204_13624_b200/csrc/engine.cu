@@ -248,7 +248,8 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
   p->zring_pf = knob("COMBO_ZRING_PF", 1);
-  p->zring_pre = knob("COMBO_ZRING_PRE", 1) != 0;
+  p->zring_pre = knob("COMBO_ZRING_PRE", 0) != 0;
+  p->zinv_regs = knob("COMBO_ZINV_REGS", 0) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -625,6 +626,10 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
         smem_attr(k, p.rzsmem + rows);
         k<<<unsigned(nb), p.rzT, p.rzsmem + rows, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL,
                                                               int(p.rzsmem / sizeof(double2)), scale, cons, part);
+      } else if (Cons::PRELOAD && L == 9 && p.rzT <= 320 && p.zinv_regs) {
+        auto k = zinv_rr<Cons, L, 320, 2>;
+        smem_attr(k, p.rzsmem);
+        k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
       } else {
         auto k = zinv_rr<Cons, L>;
         smem_attr(k, p.rzsmem);
@@ -835,6 +840,16 @@ void reset_stats(combo_ctx* c) {
 }
 
 // stress sweep: out = P(fin + sh) - alpha (fin + sh); P sums -> slot
+// COMBO_LAM_MINB: resident blocks per SM of the composite (laminate Newton)
+// kernels, i.e. their register cap (2: 255 registers, 3: 168, 4: 128)
+int lam_minb() {
+  static const int v = [] {
+    const char* s = std::getenv("COMBO_LAM_MINB");
+    return s ? std::atoi(s) : 2;
+  }();
+  return v;
+}
+
 // one rank's part: partials of its chunks, stats into the leader's counters
 void sweep_launch(combo_ctx* c, const double* fin, const Shift9& sh, double alpha, double* out, bool writeback) {
   const int64_t nb = chunk_blocks(c);
@@ -844,8 +859,15 @@ void sweep_launch(combo_ctx* c, const double* fin, const Shift9& sh, double alph
   if (c->plan && c->plan->split_sweep && fin != out) {  // pass 1 writes out before pass 2 reads fin
     if (c->ncomp > 0) {
       const unsigned g = unsigned(std::min<int64_t>((c->ncomp + 127) / 128, int64_t(c->num_sms) * 64));
-      k_sweep_comp<<<g, 128, 0, c->stream>>>(
-          c->mp, c->cell_data(), fin, sh, out, c->N, writeback ? 1 : 0, stats_ptr(c));
+      auto go = [&](auto k) {
+        k<<<g, 128, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, out, c->N, writeback ? 1 : 0, stats_ptr(c));
+      };
+      if (lam_minb() == 4)
+        go(k_sweep_comp<4>);
+      else if (lam_minb() == 3)
+        go(k_sweep_comp<3>);
+      else
+        go(k_sweep_comp<2>);
       ++c->launches;
       COMBO_CK(cudaGetLastError());
     }
@@ -878,8 +900,15 @@ void comp_tangents(combo_ctx* c, const double* F, const Shift9& sh) {
   // F gather + meta + warm read, t45 write
   ProfScope ps(c, kTagOther, double(c->ncomp) * (72.0 + 64.0 + 360.0));
   const int64_t b = (c->ncomp + 127) / 128;
-  k_comp_tangent<<<unsigned(std::min<int64_t>(b, 148 * 32)), 128, 0, c->stream>>>(c->mp, c->cell_data(), F, sh,
-                                                                                     c->t45.p, c->N);
+  auto go = [&](auto k) {
+    k<<<unsigned(std::min<int64_t>(b, 148 * 32)), 128, 0, c->stream>>>(c->mp, c->cell_data(), F, sh, c->t45.p, c->N);
+  };
+  if (lam_minb() == 4)
+    go(k_comp_tangent<4>);
+  else if (lam_minb() == 3)
+    go(k_comp_tangent<3>);
+  else
+    go(k_comp_tangent<2>);
   ++c->launches;
   COMBO_CK(cudaGetLastError());
 }

@@ -440,8 +440,10 @@ __device__ __forceinline__ void zinv_tile(const SpecView& sv, const double2* __r
   zinv_finish<Cons, L>(sm, tw, line0, nreal, npair, scale, cons, partials, slot);
 }
 
-template <class Cons, int L>
-static __global__ void __launch_bounds__(512, 2)
+// MAXT / MINB: launch bounds (512 x 2 caps the registers at 64; 320 x 2 lets a
+// PRELOAD consumer keep its prefetched values in registers at n3 = 512)
+template <class Cons, int L, int MAXT = 512, int MINB = 2>
+static __global__ void __launch_bounds__(MAXT, MINB)
     zinv_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, double scale, Cons cons,
             double* partials) {
   const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
