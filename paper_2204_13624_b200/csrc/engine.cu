@@ -247,8 +247,7 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
-  p->zring_pf = knob("COMBO_ZRING_PF", 1);
-  p->zring_pre = knob("COMBO_ZRING_PRE", 0) != 0;
+  p->zring_pre = knob("COMBO_ZRING_PRE", 1) != 0;
   p->zinv_regs = knob("COMBO_ZINV_REGS", 0) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
@@ -604,20 +603,16 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
       const size_t rows = size_t(9 * p.rzL) * size_t(p.n3p) * sizeof(double2);
       bool ring = false;
       if constexpr (L == 9) {
-        // persistent ring-staged kernel: one z-line per tile, NG consumer groups
-        auto go = [&](auto ngc) {
-          constexpr int NG = decltype(ngc)::value;
-          using Z = combo_dev::ZRing<L, NG>;
-          const int stages = int(std::min<size_t>(4, (227 * 1024 - Z::kHead - NG * Z::kWork) / rows));
-          if (stages < NG + 1) return;  // a group may run at most one ring phase ahead
-          const size_t smem = size_t(Z::kHead + NG * Z::kWork) + size_t(stages) * rows;
-          auto k = zinv_ring<Cons, L, NG>;
+        // persistent ring-staged kernel: one z-line per tile, two consumer groups
+        using Z = combo_dev::ZRing<L>;
+        const size_t smem = size_t(Z::kHead + 2 * Z::kWork) + size_t(Z::kStages) * rows;
+        if (p.zring >= 2 && p.rzL == 1 && smem <= 227 * 1024 && (!Cons::LOADS || (Cons::PRELOAD && p.zring_pre))) {
+          auto k = zinv_ring<Cons, L>;
           smem_attr(k, smem);
           const int grid = int(std::min<int64_t>(nb, c->num_sms));
-          k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, scale, cons, part, stages, p.zring_pf);
+          k<<<grid, Z::kThreads, smem, c->stream>>>(p.sv(), p.ax[2].tw.p, scale, cons, part);
           ring = true;
-        };
-        if (p.zring >= 2 && p.rzL == 1 && (!Cons::LOADS || (Cons::PRELOAD && p.zring_pre))) go(std::integral_constant<int, 2>{});
+        }
       }
       if (ring) {
       } else if (p.zbulk && p.rzsmem % 128 == 0 && p.rzsmem + rows <= 100 * 1024) {

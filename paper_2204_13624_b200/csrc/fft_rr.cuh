@@ -503,80 +503,76 @@ static __global__ void __launch_bounds__(512, 2)
   zinv_finish<Cons, L>(sm, tw, line0, nreal, npair, scale, cons, partials, blockIdx.x);
 }
 
-// Persistent ring-staged z-inverse for z-lines of 256 / 512 cells (one line
-// per tile): one block per SM; a producer lane streams the 9 spectrum rows
-// of each tile into a ring of shared-memory stages with cp.async.bulk (and
-// L2-prefetches the consumer's field rows); two consumer groups of
-// 5 N/8 threads (NG = 2 or 3) take tiles in turn -- Hermitian completion from the stage
-// into the group's pair lines, inverse stages with a named barrier over the
-// group, consumer epilogue -- so the completion / transform / epilogue phases
-// of one tile overlap the other group's and the loads of the next tiles.
+// Persistent ring-staged z-inverse for z-lines of 512 cells (one line per
+// tile): one block per SM, two consumer groups of 5 N/8 threads and no
+// producer warp (20 warps: 96 registers per thread, so a PRELOAD consumer
+// keeps its prefetched field values in registers). The 9 spectrum rows of a
+// tile reach a ring of kStages shared-memory stages by cp.async.bulk on the
+// stage's mbarrier; the group that has consumed a stage (Hermitian completion
+// into its own pair lines) re-arms it at once with the tile kStages ahead and
+// L2-prefetches that tile's consumer rows. The groups take alternate tiles,
+// so completion / inverse stages / epilogue of one tile overlap the other
+// group's and the loads in flight. armed[s] (the tile last armed on stage s)
+// keeps a group from polling a stage's barrier before its previous use was
+// re-armed -- an mbarrier only distinguishes two consecutive phases.
 // Partials are indexed by tile: same values and order as zinv_rr.
-template <int L, int NG>
+template <int L>
 struct ZRing {
   static constexpr int N = 1 << L, LS = N + N / 8, NP = 5, GT = NP * (N / 8);  // threads per consumer group
-  static constexpr int kHead = 128;
+  static constexpr int kStages = 3;
+  static constexpr int kHead = 128;           // full[kStages] barriers, armed[kStages]
   static constexpr int kWork = NP * LS * 16;  // pair lines of one group
-  static constexpr int kThreads = NG * GT + 32;
+  static constexpr int kThreads = 2 * GT;
 };
 
-// pf: who L2-prefetches the consumer's field rows -- 0 nobody, 1 the
-// producer with the tile's loads, 2 each consumer group for its next tile
-template <class Cons, int L, int NG>
-static __global__ void __launch_bounds__(ZRing<L, NG>::kThreads, 1)
-    zinv_ring(SpecView sv, const double2* __restrict__ tw, double scale, Cons cons, double* partials, int nstages,
-              int pf) {
-  using Z = ZRing<L, NG>;
-  constexpr int N = Z::N, LS = Z::LS, NP = Z::NP, GT = Z::GT;
+template <class Cons, int L>
+static __global__ void __launch_bounds__(ZRing<L>::kThreads, 1)
+    zinv_ring(SpecView sv, const double2* __restrict__ tw, double scale, Cons cons, double* partials) {
+  using Z = ZRing<L>;
+  constexpr int N = Z::N, LS = Z::LS, NP = Z::NP, GT = Z::GT, S = Z::kStages;
   extern __shared__ __align__(128) unsigned char zr_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(zr_raw);
-  uint64_t* empty = full + 8;
+  volatile long long* armed = reinterpret_cast<volatile long long*>(zr_raw + 64);
   const int n3p = int(sv.n3p), nc = int(sv.n3c);
   const int ncr = (nc + 31) & ~31;  // warp-aligned k ranges (see zfwd_rr)
   const uint32_t stage_bytes = uint32_t(9 * n3p) * 16u;
-  unsigned char* stages = zr_raw + Z::kHead + NG * Z::kWork;
+  const uint32_t rb = uint32_t(nc) * 16u;
+  unsigned char* stages = zr_raw + Z::kHead + 2 * Z::kWork;
   const int64_t ntiles = sv.ni * sv.n2;  // local z-lines
+  const int64_t stride = gridDim.x;
+  // k-th tile of this block: blockIdx.x + k stride, on stage k % S, group k % 2
+  auto arm = [&](int64_t k) {  // one thread: loads of the block's k-th tile
+    const int64_t tile = blockIdx.x + k * stride;
+    const int s = int(k % S);
+    double2* rows = reinterpret_cast<double2*>(stages + size_t(s) * stage_bytes);
+    mbar_expect_tx(&full[s], 9u * rb);
+#pragma unroll 1
+    for (int rl = 0; rl < 9; ++rl) bulk_g2s(rows + rl * n3p, sv.spec + sv.zrow(rl, tile), rb, &full[s]);
+    __threadfence_block();
+    armed[s] = k;
+#pragma unroll 1
+    for (int c = 0; c < 9; ++c) cons.prefetch(c, tile * N, N);
+  };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < nstages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], GT / 32);
+      armed[s] = -1;
     }
     mbar_fence_init();
+    for (int64_t k = 0; k < S && blockIdx.x + k * stride < ntiles; ++k) arm(k);
   }
   __syncthreads();
-  if (int(threadIdx.x) >= NG * GT) {  // producer warp
-    if ((threadIdx.x & 31) == 0) {
-      Ring rg(nstages);
-      int k = 0;
-      const uint32_t rb = uint32_t(nc) * 16u;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k, rg.next()) {
-        if (k >= nstages) mbar_wait(&empty[rg.s], rg.phase ^ 1u);
-        double2* rows = reinterpret_cast<double2*>(stages + size_t(rg.s) * stage_bytes);
-        mbar_expect_tx(&full[rg.s], 9u * rb);
-#pragma unroll 1
-        for (int rl = 0; rl < 9; ++rl) bulk_g2s(rows + rl * n3p, sv.spec + sv.zrow(rl, tile), rb, &full[rg.s]);
-        if (pf == 1) {
-#pragma unroll 1
-          for (int c = 0; c < 9; ++c) cons.prefetch(c, tile * N, N);
-        }
-      }
-    }
-    return;
-  }
   const int g = int(threadIdx.x) / GT, tid = int(threadIdx.x) - g * GT;
   const GroupSync gsync{1 + g, GT};
   double2* work = reinterpret_cast<double2*>(zr_raw + Z::kHead + g * Z::kWork);
-  Ring rg(nstages);
-  int k = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k, rg.next()) {
-    if (k % NG != g) continue;
-    if (pf == 2 && tid < 9) {
-      const int64_t nxt = tile + int64_t(NG) * gridDim.x;
-      if (nxt < ntiles) cons.prefetch(tid, nxt * N, N);
-    }
+  for (int64_t k = g; blockIdx.x + k * stride < ntiles; k += 2) {
+    const int64_t tile = blockIdx.x + k * stride;
+    const int s = int(k % S);
     gsync();  // the previous tile's reduction has left the pair lines
-    mbar_wait(&full[rg.s], rg.phase);
-    const double2* rows = reinterpret_cast<const double2*>(stages + size_t(rg.s) * stage_bytes);
+    while (armed[s] != k) {
+    }
+    mbar_wait(&full[s], uint32_t((k / S) & 1));
+    const double2* rows = reinterpret_cast<const double2*>(stages + size_t(s) * stage_bytes);
     // Hermitian completion of the pairs (see zinv_tile) from the staged rows
     for (int t = tid; t < NP * ncr; t += GT) {
       const int pp = t / ncr, kk = t - pp * ncr;
@@ -593,7 +589,7 @@ static __global__ void __launch_bounds__(ZRing<L, NG>::kThreads, 1)
       if (!selfconj) work[pp * LS + pad8(N - kk)] = make_double2(xa.x + xb.y, xb.x - xa.y);
     }
     gsync();  // stage consumed, pair lines complete
-    if ((tid & 31) == 0) mbar_arrive(&empty[rg.s]);
+    if (tid == 0 && blockIdx.x + (k + S) * stride < ntiles) arm(k + S);
     zinv_finish<Cons, L>(work, tw, tile, 9, NP, scale, cons, partials, tile, tid, GT, gsync);
   }
 }

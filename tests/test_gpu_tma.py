@@ -68,11 +68,11 @@ def test_tma_fft_forward_vs_numpy(ctx):
     assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("dims", [(16, 8, 512), (8, 8, 64), (4, 12, 256)])
+@pytest.mark.parametrize("dims", [(16, 8, 512), (32, 40, 512), (8, 8, 64), (4, 12, 256)])
 def test_zinv_staged_variants_bitwise_equal_register_loads(dims):
     """zinv_ring (persistent, spectrum rows through a cp.async.bulk ring, two
-    consumer groups; n3 = 512) and zinv_bulk (rows staged per block) against
-    zinv_rr."""
+    consumer groups; n3 = 512; 1280 tiles: every block re-arms its stages) and
+    zinv_bulk (rows staged per block) against zinv_rr."""
     rng = np.random.default_rng(21)
     tau = rng.uniform(-1, 1, 9 * int(np.prod(dims)))
     outs = []
@@ -94,7 +94,7 @@ def test_zinv_ring_solve_bitwise(oracle, scheme, green):
     one-block-per-tile kernel, P-bar within 1e-9 of the oracle."""
     import paper_2204_13624_b200 as pkg
 
-    fine, fac = (16, 24, 1024), (4, 4, 2)
+    fine, fac = (128, 96, 1024), (4, 4, 2)  # 32 x 24 x 512 grid: 768 z-line tiles, 5-6 per block
     dims = tuple(f // k for f, k in zip(fine, fac))
     fbar = np.eye(3)
     fbar[0, 0] += 0.04
@@ -103,11 +103,11 @@ def test_zinv_ring_solve_bitwise(oracle, scheme, green):
     for ring in (2, 0):
         c, old = _fresh_ctx(COMBO_ZRING=ring)
         try:
-            img = c.generate("rsa_spheres", fine, (1, 1, 1), 3, 3.0, 6.0, 0.3)
+            img = c.generate("rsa_spheres", fine, (1, 1, 1), 3, 6.0, 12.0, 0.3)
             kind, cp, _ = c.coarsen(img, fac)
             nrm, _, _ = c.compute_normals(img, fac, kind)
             cm = pkg.CellMaterials(c, dims, kind, cp, nrm, pkg.neo_hookean(2.0, 1.0), pkg.neo_hookean(20.0, 10.0))
-            runs.append((cm.solve(fbar, scheme=scheme, green=green, tol_equilibrium=1e-7, load_steps=2,
+            runs.append((cm.solve(fbar, scheme=scheme, green=green, tol_equilibrium=1e-6, load_steps=1,
                                   max_outer=2000), (kind, cp, nrm)))
         finally:
             _restore(old)
@@ -122,7 +122,7 @@ def test_zinv_ring_solve_bitwise(oracle, scheme, green):
     kind, cp, nrm = grid
     cmo = oracle.CellMaterials(dims, kind, cp, nrm, oracle.neo_hookean(2.0, 1.0), oracle.neo_hookean(20.0, 10.0))
     ro = cmo.solve(fbar, scheme=1 if scheme == "newton_cg" else 0, green={"rotated": 1, "continuous": 0}[green],
-                   tol=1e-7, load_steps=2, max_outer=2000)
+                   tol=1e-6, load_steps=1, max_outer=2000)
     assert np.linalg.norm(a["pbar"] - ro["pbar"]) <= 1e-9 * np.linalg.norm(ro["pbar"])
 
 
