@@ -835,13 +835,19 @@ void reset_stats(combo_ctx* c) {
 }
 
 // stress sweep: out = P(fin + sh) - alpha (fin + sh); P sums -> slot
-// COMBO_LAM_MINB: resident blocks per SM of the composite (laminate Newton)
-// kernels, i.e. their register cap (2: 255 registers, 3: 168, 4: 128)
-int lam_minb() {
-  static const int v = [] {
-    const char* s = std::getenv("COMBO_LAM_MINB");
-    return s ? std::atoi(s) : 2;
-  }();
+// Resident blocks per SM of the composite (laminate Newton) kernels, i.e.
+// their register cap (2: 255 registers, 3: 168, 4: 128). Measured at 512^3
+// (profiles/r2m_*): sweep 49.8 / 41.1 / 40.0 ms, tangents 32.2 / 32.2 / 38.0 ms.
+int knob_int(const char* name, int dflt) {
+  const char* s = std::getenv(name);
+  return s ? std::atoi(s) : dflt;
+}
+int sweep_minb() {
+  static const int v = knob_int("COMBO_SWEEP_MINB", 3);
+  return v;
+}
+int tangent_minb() {
+  static const int v = knob_int("COMBO_TANGENT_MINB", 2);
   return v;
 }
 
@@ -857,9 +863,9 @@ void sweep_launch(combo_ctx* c, const double* fin, const Shift9& sh, double alph
       auto go = [&](auto k) {
         k<<<g, 128, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, out, c->N, writeback ? 1 : 0, stats_ptr(c));
       };
-      if (lam_minb() == 4)
+      if (sweep_minb() == 4)
         go(k_sweep_comp<4>);
-      else if (lam_minb() == 3)
+      else if (sweep_minb() == 3)
         go(k_sweep_comp<3>);
       else
         go(k_sweep_comp<2>);
@@ -898,9 +904,9 @@ void comp_tangents(combo_ctx* c, const double* F, const Shift9& sh) {
   auto go = [&](auto k) {
     k<<<unsigned(std::min<int64_t>(b, 148 * 32)), 128, 0, c->stream>>>(c->mp, c->cell_data(), F, sh, c->t45.p, c->N);
   };
-  if (lam_minb() == 4)
+  if (tangent_minb() == 4)
     go(k_comp_tangent<4>);
-  else if (lam_minb() == 3)
+  else if (tangent_minb() == 3)
     go(k_comp_tangent<3>);
   else
     go(k_comp_tangent<2>);

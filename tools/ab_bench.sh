@@ -2,7 +2,7 @@
 # runs the default bench workload for 1 timed step, no CPU / e2e legs.
 tag=$1; shift
 mkdir -p gpurun_out
-env "$@" python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ab_$tag.log 2>&1
+env "$@" timeout 900 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ab_$tag.log 2>&1
 python - "$tag" <<'PY'
 import json, sys
 tag = sys.argv[1]
