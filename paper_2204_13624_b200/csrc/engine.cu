@@ -247,7 +247,7 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   p->zbulk = knob("COMBO_ZBULK", 0) != 0;
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
-  p->zring_pre = knob("COMBO_ZRING_PRE", 1) != 0;
+  p->zring_pre = knob("COMBO_ZRING_PRE", 0) != 0;
   p->zinv_regs = knob("COMBO_ZINV_REGS", 0) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
