@@ -119,7 +119,6 @@ struct FftPlan {
   bool zring_pre = false;  // ring also for PRELOAD consumers (COMBO_ZRING_PRE=1; measured slower: 8.8 vs 7.5 ms)
   bool zinv_regs = false;  // PRELOAD consumers at n3 = 512: 320 x 2 launch bounds, no spills (COMBO_ZINV_REGS=1)
   bool tma_x = false, tma_y = false;
-  bool tma_x2 = false;  // x + Gamma with one channel per thread (COMBO_XTMA2=1)
   int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
   CUtensorMap xmap{}, ymap{};
   // slab decomposition (R ranks, this plan's rank q): planes [i0, i0 + ni)

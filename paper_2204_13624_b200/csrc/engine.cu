@@ -297,7 +297,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     if (knob("COMBO_XTMA", 1) != 0 && pow2_between(d[0], 6, 10)) {
       p->tma_x_line_first = encode_strip_map(&p->xmap, *p, true, combo_dev::kTmaW);
       p->tma_x = true;
-      p->tma_x2 = knob("COMBO_XTMA2", 0) != 0;
     }
     if (knob("COMBO_YTMA", 1) != 0 && pow2_between(d[1], 6, 10)) {
       p->tma_yw = d[1] >= 1024 ? 4 : 8;
@@ -701,22 +700,6 @@ void launch_xgamma(combo_ctx* c, int kind, int rg0 = 0, int nrg = 3) {
           smem_attr(k, smem);
           k<<<grid, int(p.dims[0] / 8) * W, smem, c->stream>>>(p.xmap, p.svB(), p.ax[0].tw.p, g, p.tma_x_line_first);
         };
-        if constexpr (L <= 9) {
-          if (p.tma_x2) {  // one channel per thread, twice the threads
-            auto go2 = [&](auto k) {
-              smem_attr(k, smem);
-              k<<<grid, 2 * int(p.dims[0] / 8) * W, smem, c->stream>>>(p.xmap, p.svB(), p.ax[0].tw.p, g,
-                                                                       p.tma_x_line_first);
-            };
-            if (kind == 0)
-              go2(xgamma_tma2<L, 0>);
-            else if (kind == 1)
-              go2(xgamma_tma2<L, 1>);
-            else
-              go2(xgamma_tma2<L, 2>);
-            return;
-          }
-        }
         if (kind == 0)
           go(xgamma_tma<L, 0>);
         else if (kind == 1)

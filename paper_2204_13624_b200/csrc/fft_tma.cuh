@@ -140,112 +140,6 @@ static __global__ void __launch_bounds__((1 << L) / 8 * kTmaW, (1 << L) <= 512 ?
   }
 }
 
-// Same pass with one channel per thread: 2 x W x N/8 threads, the first half
-// transforms component 0, the second half the combination e_1 t_1 + e_2 t_2;
-// the halves swap their spectra through the buffer around the Gamma step.
-// Twice the warps per tile at half the registers (64), same arithmetic per
-// channel as xgamma_tma (bitwise).
-template <int L, int KIND>
-static __global__ void __launch_bounds__((1 << L) / 8 * kTmaW * 2, (1 << L) <= 512 ? 2 : 1)
-    xgamma_tma2(const __grid_constant__ CUtensorMap map, SpecView sv, const double2* __restrict__ tw, GreenTables G,
-                int lineFirst) {
-  constexpr int N = 1 << L, W = kTmaW, RB = TmaRows<N>::RB, NB = TmaRows<N>::NB, HT = N / 8 * W;
-  extern __shared__ __align__(128) double2 sm[];
-  __shared__ uint64_t bar;
-  const int rg = blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
-  const int w = min(W, int(sv.n3c) - kc0);
-  const int half = int(threadIdx.x) / HT, t = int(threadIdx.x) - half * HT;
-  const int line = t % W, u = t / W;
-  const bool active = line < w;
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&map);
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-    mbar_expect_tx(&bar, uint32_t(3 * N * W * sizeof(double2)));
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      if (lineFirst)
-        tma_load_4d(sm + b * 3 * RB * W, &map, &bar, 2 * kc0, b * RB, j, 3 * rg);
-      else
-        tma_load_4d(sm + b * 3 * RB * W, &map, &bar, 2 * kc0, j, b * RB, 3 * rg);
-    }
-  }
-  // the column factors are re-derived in each phase that needs them (L1-hot
-  // table loads) instead of living in 16 registers across the stages; the
-  // opaque copy of the column index keeps the compiler from merging them
-  auto column = [&]() {
-    int k3 = kc0 + line;
-    asm volatile("" : "+r"(k3));
-    return rank_col<KIND>(G, rg, sv.j0 + j, k3, sv.n2, sv.n3);
-  };
-  __syncthreads();  // barrier initialised before anyone polls it
-  mbar_wait(&bar, 0);
-  auto tile = [&](int comp, int pos) { return ((pos / RB * 3 + comp) * RB + pos % RB) * W + line; };
-  double2 v[1][8];
-  if (active) {
-    const RankCol<KIND> col = column();
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int pos = rr_first_pos<L, false>(u, q);
-      if (half == 0) {
-        v[0][q] = sm[tile(0, pos)];
-      } else {
-        const double2 a = cmulc(col.o1, sm[tile(1, pos)]), b = cmulc(col.o2, sm[tile(2, pos)]);
-        v[0][q] = make_double2(a.x + b.x, a.y + b.y);
-      }
-    }
-  }
-  __syncthreads();  // the exchanges below overwrite the input tile
-  constexpr int chs = (N + N / 8) * W;
-  auto addr = [&](int, int pos) { return half * chs + pad8(pos) * W + line; };
-  rr_stages<L, false, false, 0, 1>(v, u, active, sm, tw, addr);
-  // Gamma needs both channels at a frequency: swap the spectra via the buffer
-  if (active) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) sm[addr(0, rr_final_pos<L, false>(u, q))] = v[0][q];
-  }
-  __syncthreads();
-  if (active) {
-    const RankCol<KIND> col = column();
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int pos = rr_final_pos<L, false>(u, q);
-      const double2 other = sm[(1 - half) * chs + pad8(pos) * W + line];
-      double2 t0 = half == 0 ? v[0][q] : other, uu = half == 0 ? other : v[0][q];
-      rank_gamma<KIND>(G, col, rg, pos, sv.n1, t0, uu);
-      v[0][q] = half == 0 ? t0 : uu;
-    }
-  }
-  __syncthreads();  // partners have read before the inverse exchanges overwrite
-  rr_stages<L, true, true, 0, 1>(v, u, active, sm, tw, addr);
-  // every thread is past the last exchange barrier: the buffer is free
-  if (active) {
-    const RankCol<KIND> col = column();
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int pos = rr_final_pos<L, true>(u, q);
-      if (half == 0) {
-        sm[tile(0, pos)] = v[0][q];
-      } else {
-        sm[tile(1, pos)] = cmul(col.o1, v[0][q]);
-        sm[tile(2, pos)] = cmul(col.o2, v[0][q]);
-      }
-    }
-  }
-  fence_proxy_async_smem();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      if (lineFirst)
-        tma_store_4d(&map, sm + b * 3 * RB * W, 2 * kc0, b * RB, j, 3 * rg);
-      else
-        tma_store_4d(&map, sm + b * 3 * RB * W, 2 * kc0, j, b * RB, 3 * rg);
-    }
-    tma_store_commit_wait();
-  }
-}
-
 // ------------------------------------------------------------------ Y pass
 // Tile: N rows (k2) x W columns of component c on local plane i (box
 // component extent 1). Same buffer discipline as above with one channel.

@@ -37,8 +37,7 @@ def test_tma_passes_bitwise_equal_register_passes(dims, lengths, kind):
     tau = rng.uniform(-1, 1, 9 * int(np.prod(dims)))
     outs = []
     for knobs in (dict(COMBO_XTMA=1, COMBO_YTMA=1), dict(COMBO_XTMA=0, COMBO_YTMA=0),
-                  dict(COMBO_XTMA=1, COMBO_YTMA=1, COMBO_YTMA_W=4), dict(COMBO_XTMA=1, COMBO_YTMA=1, COMBO_SWAP=0),
-                  dict(COMBO_XTMA=1, COMBO_XTMA2=1), dict(COMBO_XTMA=1, COMBO_XTMA2=1, COMBO_SWAP=0)):
+                  dict(COMBO_XTMA=1, COMBO_YTMA=1, COMBO_YTMA_W=4), dict(COMBO_XTMA=1, COMBO_YTMA=1, COMBO_SWAP=0)):
         c, old = _fresh_ctx(**knobs)
         try:
             # plans read the knobs when the grid is set
