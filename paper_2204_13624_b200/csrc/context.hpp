@@ -112,12 +112,9 @@ struct FftPlan {
   bool pq_dot = true;    // CG: pdir^T A pdir summed in the matvec (COMBO_PQ=0: in the z-inverse consumer)
   // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
   // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off
-  bool zbulk = false;  // z-inverse with spectrum rows staged per block (COMBO_ZBULK=1; measured slower: 2 blocks/SM)
   // persistent ring-staged z-inverse at n3 = 512 (two consumer groups; COMBO_ZRING=0: one block per
   // tile), used for consumers whose epilogue reads no field (Cons::LOADS)
   int zring = 2;
-  bool zring_pre = false;  // ring also for PRELOAD consumers (COMBO_ZRING_PRE=1; measured slower: 8.8 vs 7.5 ms)
-  bool zinv_regs = false;  // PRELOAD consumers at n3 = 512: 320 x 2 launch bounds, no spills (COMBO_ZINV_REGS=1)
   bool tma_x = false, tma_y = false;
   int tma_x_line_first = 1, tma_y_line_first = 0, tma_yw = 8;
   CUtensorMap xmap{}, ymap{};

@@ -244,11 +244,8 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
     return v ? std::atoi(v) : dflt;
   };
   p->xminb = knob("COMBO_XMINB", 2);
-  p->zbulk = knob("COMBO_ZBULK", 0) != 0;
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
   p->zring = knob("COMBO_ZRING", 2);
-  p->zring_pre = knob("COMBO_ZRING_PRE", 0) != 0;
-  p->zinv_regs = knob("COMBO_ZINV_REGS", 0) != 0;
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
   // register-resident geometry (pow2 axes >= 8): T = lines * N/8
@@ -506,23 +503,6 @@ void dispatch_log2(int64_t n, F&& f) {
   }
 }
 
-// COMBO_PF = waves of resident blocks a column-strip pass prefetches ahead
-// into L2 (0: off)
-int pf_waves() {
-  static const int v = [] {
-    const char* s = std::getenv("COMBO_PF");
-    return s ? std::atoi(s) : 0;
-  }();
-  return v;
-}
-template <class K>
-int ahead_blocks(const combo_ctx* c, K kernel, int threads, size_t smem) {
-  if (pf_waves() <= 0) return 0;
-  int occ = 0;
-  COMBO_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
-  return pf_waves() * std::max(occ, 1) * c->num_sms;
-}
-
 // CG matvec: bulk-staged persistent kernel (one CTA per SM) when the rows
 // are 16-byte aligned, else one cell per thread with direct loads.
 template <bool FIRST, bool HASX>
@@ -606,7 +586,7 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
         // persistent ring-staged kernel: one z-line per tile, two consumer groups
         using Z = combo_dev::ZRing<L>;
         const size_t smem = size_t(Z::kHead + 2 * Z::kWork) + size_t(Z::kStages) * rows;
-        if (p.zring >= 2 && p.rzL == 1 && smem <= 227 * 1024 && (!Cons::LOADS || (Cons::PRELOAD && p.zring_pre))) {
+        if (p.zring >= 2 && p.rzL == 1 && smem <= 227 * 1024 && !Cons::LOADS) {
           auto k = zinv_ring<Cons, L>;
           smem_attr(k, smem);
           const int grid = int(std::min<int64_t>(nb, c->num_sms));
@@ -615,16 +595,6 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
         }
       }
       if (ring) {
-      } else if (p.zbulk && p.rzsmem % 128 == 0 && p.rzsmem + rows <= 100 * 1024) {
-        // spectrum rows staged by cp.async.bulk behind the pair lines
-        auto k = zinv_bulk<Cons, L>;
-        smem_attr(k, p.rzsmem + rows);
-        k<<<unsigned(nb), p.rzT, p.rzsmem + rows, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL,
-                                                              int(p.rzsmem / sizeof(double2)), scale, cons, part);
-      } else if (Cons::PRELOAD && L == 9 && p.rzT <= 320 && p.zinv_regs) {
-        auto k = zinv_rr<Cons, L, 320, 2>;
-        smem_attr(k, p.rzsmem);
-        k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
       } else {
         auto k = zinv_rr<Cons, L>;
         smem_attr(k, p.rzsmem);
@@ -672,7 +642,7 @@ void launch_y(combo_ctx* c, int ncomp = 9, int c0 = 0) {
       dim3 grid(unsigned((p.n3c + p.ryW - 1) / p.ryW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_rr<L, INV>;
       smem_attr(k, p.rysmem);
-      k<<<grid, p.ryT, p.rysmem, c->stream>>>(svy, p.ax[1].tw.p, p.ryW, ahead_blocks(c, k, p.ryT, p.rysmem));
+      k<<<grid, p.ryT, p.rysmem, c->stream>>>(svy, p.ax[1].tw.p, p.ryW);
     } else {
       dim3 grid(unsigned((p.n3c + p.yW - 1) / p.yW), unsigned(p.ni), unsigned(ncomp));
       auto k = ypass_kernel<L, INV>;
@@ -714,8 +684,7 @@ void launch_xgamma(combo_ctx* c, int kind, int rg0 = 0, int nrg = 3) {
       dim3 grid(unsigned((p.n3c + p.rxW - 1) / p.rxW), unsigned(p.nj), unsigned(nrg));
       auto go = [&](auto k) {
         smem_attr(k, p.rxsmem);
-        k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g, ahead_blocks(c, k, p.rxT, p.rxsmem),
-                                               rg0);
+        k<<<grid, p.rxT, p.rxsmem, c->stream>>>(p.svB(), p.ax[0].tw.p, p.rxW, g, rg0);
       };
       auto by_kind = [&](auto k0, auto k1, auto k2) {
         if (kind == 0)
@@ -835,22 +804,6 @@ void reset_stats(combo_ctx* c) {
 }
 
 // stress sweep: out = P(fin + sh) - alpha (fin + sh); P sums -> slot
-// Resident blocks per SM of the composite (laminate Newton) kernels, i.e.
-// their register cap (2: 255 registers, 3: 168, 4: 128). Measured at 512^3
-// (profiles/r2m_*): sweep 49.8 / 41.1 / 40.0 ms, tangents 32.2 / 32.2 / 38.0 ms.
-int knob_int(const char* name, int dflt) {
-  const char* s = std::getenv(name);
-  return s ? std::atoi(s) : dflt;
-}
-int sweep_minb() {
-  static const int v = knob_int("COMBO_SWEEP_MINB", 3);
-  return v;
-}
-int tangent_minb() {
-  static const int v = knob_int("COMBO_TANGENT_MINB", 2);
-  return v;
-}
-
 // one rank's part: partials of its chunks, stats into the leader's counters
 void sweep_launch(combo_ctx* c, const double* fin, const Shift9& sh, double alpha, double* out, bool writeback) {
   const int64_t nb = chunk_blocks(c);
@@ -860,15 +813,8 @@ void sweep_launch(combo_ctx* c, const double* fin, const Shift9& sh, double alph
   if (c->plan && c->plan->split_sweep && fin != out) {  // pass 1 writes out before pass 2 reads fin
     if (c->ncomp > 0) {
       const unsigned g = unsigned(std::min<int64_t>((c->ncomp + 127) / 128, int64_t(c->num_sms) * 64));
-      auto go = [&](auto k) {
-        k<<<g, 128, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, out, c->N, writeback ? 1 : 0, stats_ptr(c));
-      };
-      if (sweep_minb() == 4)
-        go(k_sweep_comp<4>);
-      else if (sweep_minb() == 3)
-        go(k_sweep_comp<3>);
-      else
-        go(k_sweep_comp<2>);
+      k_sweep_comp<<<g, 128, 0, c->stream>>>(c->mp, c->cell_data(), fin, sh, out, c->N, writeback ? 1 : 0,
+                                             stats_ptr(c));
       ++c->launches;
       COMBO_CK(cudaGetLastError());
     }
@@ -901,15 +847,8 @@ void comp_tangents(combo_ctx* c, const double* F, const Shift9& sh) {
   // F gather + meta + warm read, t45 write
   ProfScope ps(c, kTagOther, double(c->ncomp) * (72.0 + 64.0 + 360.0));
   const int64_t b = (c->ncomp + 127) / 128;
-  auto go = [&](auto k) {
-    k<<<unsigned(std::min<int64_t>(b, 148 * 32)), 128, 0, c->stream>>>(c->mp, c->cell_data(), F, sh, c->t45.p, c->N);
-  };
-  if (tangent_minb() == 4)
-    go(k_comp_tangent<4>);
-  else if (tangent_minb() == 3)
-    go(k_comp_tangent<3>);
-  else
-    go(k_comp_tangent<2>);
+  k_comp_tangent<<<unsigned(std::min<int64_t>(b, 148 * 32)), 128, 0, c->stream>>>(c->mp, c->cell_data(), F, sh,
+                                                                                     c->t45.p, c->N);
   ++c->launches;
   COMBO_CK(cudaGetLastError());
 }

@@ -177,23 +177,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-// Wave-ahead L2 prefetch of a column-strip tile: the block `ahead` launch
-// positions after this one (about one wave of resident blocks later) gets
-// its rows into L2 now, so its loads see L2 instead of DRAM latency. The
-// grid is (column blocks, lines, channel groups); rows(b1, b2, t) gives the
-// address of the t-th row segment of block (x = b0, y = b1, z = b2).
-template <class Rows>
-__device__ __forceinline__ void prefetch_ahead(int ahead, int nrows, const Rows& rows) {
-  if (ahead <= 0) return;
-  const int64_t nb = int64_t(gridDim.x) * gridDim.y * gridDim.z;
-  const int64_t b = blockIdx.x + int64_t(gridDim.x) * (blockIdx.y + int64_t(gridDim.y) * blockIdx.z) + ahead;
-  if (b >= nb) return;
-  const int b0 = int(b % gridDim.x);
-  const int64_t r = b / gridDim.x;
-  const int b1 = int(r % gridDim.y), b2 = int(r / gridDim.y);
-  for (int t = threadIdx.x; t < nrows; t += blockDim.x) prefetch_l2(rows(b0, b1, b2, t));
-}
-
 // ---------------------------------------------------------------- reductions
 // Threads are grouped in power-of-two groups of G lanes sharing the same
 // (component a, component b) pair; per group: NSC scalars, plus per-component
@@ -440,67 +423,14 @@ __device__ __forceinline__ void zinv_tile(const SpecView& sv, const double2* __r
   zinv_finish<Cons, L>(sm, tw, line0, nreal, npair, scale, cons, partials, slot);
 }
 
-// MAXT / MINB: launch bounds (512 x 2 caps the registers at 64; 320 x 2 lets a
-// PRELOAD consumer keep its prefetched values in registers at n3 = 512)
-template <class Cons, int L, int MAXT = 512, int MINB = 2>
-static __global__ void __launch_bounds__(MAXT, MINB)
+template <class Cons, int L>
+static __global__ void __launch_bounds__(512, 2)
     zinv_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, double scale, Cons cons,
             double* partials) {
   const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
   zinv_tile<Cons, L>(sv, tw, line0, int(min(int64_t(nl_per_block), nlines_tot - line0)), scale, cons, partials,
                      blockIdx.x);
-}
-
-// Bulk-staged z-inverse: one thread fetches the tile's spectrum rows (n3c
-// complex each, contiguous) with cp.async.bulk into shared memory behind the
-// pair lines; the Hermitian completion then reads shared memory, so no warp
-// waits on HBM loads in registers. rows_off = offset of the row buffer in sm.
-template <class Cons, int L>
-static __global__ void __launch_bounds__(512, 2)
-    zinv_bulk(SpecView sv, const double2* __restrict__ tw, int nl_per_block, int rows_off, double scale, Cons cons,
-              double* partials) {
-  constexpr int N = 1 << L, LS = N + N / 8;
-  extern __shared__ __align__(128) double2 sm[];
-  __shared__ uint64_t bar;
-  const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
-  const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
-  const int nlines = int(min(int64_t(nl_per_block), nlines_tot - line0));
-  const int nreal = 9 * nlines;
-  const int npair = (nreal + 1) >> 1;
-  const int nc = int(sv.n3c);
-  const int ncr = (nc + 31) & ~31;  // warp-aligned k ranges (see zfwd_rr)
-  double2* rows = sm + rows_off;
-  const int n3p = int(sv.n3p);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-    const uint32_t rb = uint32_t(nc) * 16u;
-    mbar_expect_tx(&bar, rb * uint32_t(nreal));
-    for (int rl = 0; rl < nreal; ++rl)
-      bulk_g2s(rows + rl * n3p, sv.spec + sv.zrow(rl % 9, line0 + rl / 9), rb, &bar);
-  }
-  if (threadIdx.x >= 32 && threadIdx.x < 41) cons.prefetch(int(threadIdx.x) - 32, line0 * N, int64_t(nlines) * N);
-  __syncthreads();  // barrier initialised before anyone polls it
-  mbar_wait(&bar, 0);
-  // Hermitian completion of the pair (halfcomplex c2r: DC/Nyquist imaginary
-  // parts ignored) into natural-order smem lines
-  for (int t = threadIdx.x; t < npair * ncr; t += blockDim.x) {
-    const int pp = t / ncr, k = t - pp * ncr;
-    if (k >= nc) continue;
-    const int rl = 2 * pp;
-    double2 xa = rows[rl * n3p + k];
-    double2 xb = rl + 1 < nreal ? rows[(rl + 1) * n3p + k] : make_double2(0.0, 0.0);
-    const bool selfconj = (k == 0) || (2 * k == N);
-    if (selfconj) {
-      xa.y = 0.0;
-      xb.y = 0.0;
-    }
-    sm[pp * LS + pad8(k)] = make_double2(xa.x - xb.y, xa.y + xb.x);
-    if (!selfconj) sm[pp * LS + pad8(N - k)] = make_double2(xa.x + xb.y, xb.x - xa.y);
-  }
-  __syncthreads();
-  zinv_finish<Cons, L>(sm, tw, line0, nreal, npair, scale, cons, partials, blockIdx.x);
 }
 
 // Persistent ring-staged z-inverse for z-lines of 512 cells (one line per
@@ -599,12 +529,9 @@ static __global__ void __launch_bounds__(ZRing<L>::kThreads, 1)
 // one tile: columns [kc0, kc0 + W) of component c, local plane i
 template <int L, bool INV, bool CG = false>
 __device__ __forceinline__ void ypass_tile(const SpecView& sv, const double2* __restrict__ tw, int W, int c,
-                                           int64_t i, int kc0, int ahead = 0) {
+                                           int64_t i, int kc0) {
   constexpr int N = 1 << L;
   extern __shared__ double2 sm[];
-  prefetch_ahead(ahead, N, [&](int b0, int b1, int b2, int t) {
-    return sv.spec + int64_t(b2) * sv.cs + b0 * W + sv.rowA(b1, t);
-  });
   const int w = min(W, int(sv.n3c) - kc0);
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
@@ -627,8 +554,8 @@ __device__ __forceinline__ void ypass_tile(const SpecView& sv, const double2* __
 
 template <int L, bool INV, int MAXT = 512, int MINB = 2>
 static __global__ void __launch_bounds__(MAXT, MINB)
-    ypass_rr(SpecView sv, const double2* __restrict__ tw, int W, int ahead) {
-  ypass_tile<L, INV>(sv, tw, W, blockIdx.z, blockIdx.y, blockIdx.x * W, ahead);
+    ypass_rr(SpecView sv, const double2* __restrict__ tw, int W) {
+  ypass_tile<L, INV>(sv, tw, W, blockIdx.z, blockIdx.y, blockIdx.x * W);
 }
 
 // ---------------------------------------------------------------- X + Gamma
@@ -728,7 +655,7 @@ __device__ __forceinline__ void rank_gamma(const GreenTables& G, const RankCol<K
 
 template <int L, int KIND, int MAXT, int MINB>
 static __global__ void __launch_bounds__(MAXT, MINB)
-    xgamma_v4(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G, int ahead, int rg0) {
+    xgamma_v4(SpecView sv, const double2* __restrict__ tw, int W, GreenTables G, int rg0) {
   constexpr int N = 1 << L;
   extern __shared__ double2 sm[];
   const int rg = rg0 + blockIdx.z, j = blockIdx.y, kc0 = blockIdx.x * W;
@@ -736,9 +663,6 @@ static __global__ void __launch_bounds__(MAXT, MINB)
   const int line = threadIdx.x % W, u = threadIdx.x / W;
   const bool active = line < w && u < N / 8;
   const int64_t plane = sv.cs;
-  prefetch_ahead(ahead, 3 * N, [&](int b0, int b1, int b2, int t) {
-    return sv.spec + int64_t(3 * (rg0 + b2) + t / N) * plane + b0 * W + sv.rowB(t % N, b1);
-  });
   double2* base = sv.spec + int64_t(3 * rg) * plane + kc0 + line;  // pencil side, local k2 j
   const RankCol<KIND> col = rank_col<KIND>(G, rg, sv.j0 + j, kc0 + line, sv.n2, sv.n3);
   double2 v[2][8];

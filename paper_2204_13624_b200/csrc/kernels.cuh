@@ -146,9 +146,9 @@ static __global__ void __launch_bounds__(kEwThreads) k_sweep(MatParams M, CellDa
 // thread over the compact composite list, so the per-cell Newton no longer
 // serialises the pure cells of mixed warps. Writes the raw P of each
 // composite cell (0 when inadmissible) into out; pass 2 folds it in.
-// MINB blocks of 128 threads per SM bound the registers (2: 255, 3: 168, 4: 128)
-template <int MINB>
-static __global__ void __launch_bounds__(128, MINB)
+// 3 blocks of 128 threads per SM (168 registers): 41.1 ms per sweep at 512^3
+// against 49.8 ms at 2 blocks (255 registers) and 40.0 ms at 4 (128)
+static __global__ void __launch_bounds__(128, 3)
     k_sweep_comp(MatParams M, CellData cd, const double* __restrict__ fin, Shift9 sh, double* __restrict__ out,
                  int64_t N, int writeback, Stats* st) {
   unsigned long long inad = 0, fail = 0, bp = 0;
@@ -538,8 +538,8 @@ static __global__ void __launch_bounds__(kMvT + 32, 1) k_matvec_bulk(MatvecArgs 
 // Packed effective tangents of all composite cells at (F, warm starts): the
 // tangent half of stress_sweep(tangents45) (cell_material.cpp:146-160),
 // evaluated once per Newton iteration.
-template <int MINB>
-static __global__ void __launch_bounds__(128, MINB)
+// 2 blocks per SM (255 registers): 32.2 ms at 512^3; 3 blocks 32.2, 4 blocks 38.0
+static __global__ void __launch_bounds__(128, 2)
     k_comp_tangent(MatParams M, CellData cd, const double* __restrict__ fin, Shift9 sh, double* __restrict__ t45,
                    int64_t N) {
   for (int64_t id = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; id < cd.ncomp;

@@ -69,14 +69,14 @@ def test_tma_fft_forward_vs_numpy(ctx):
 
 
 @pytest.mark.parametrize("dims", [(16, 8, 512), (32, 40, 512), (8, 8, 64), (4, 12, 256)])
-def test_zinv_staged_variants_bitwise_equal_register_loads(dims):
+def test_zinv_ring_bitwise_equal_register_loads(dims):
     """zinv_ring (persistent, spectrum rows through a cp.async.bulk ring, two
-    consumer groups; n3 = 512; 1280 tiles: every block re-arms its stages) and
-    zinv_bulk (rows staged per block) against zinv_rr."""
+    consumer groups; n3 = 512; 1280 tiles: every block re-arms its stages)
+    against zinv_rr."""
     rng = np.random.default_rng(21)
     tau = rng.uniform(-1, 1, 9 * int(np.prod(dims)))
     outs = []
-    for knobs in (dict(COMBO_ZRING=2), dict(COMBO_ZRING=0, COMBO_ZBULK=0), dict(COMBO_ZRING=0, COMBO_ZBULK=1)):
+    for knobs in (dict(COMBO_ZRING=2), dict(COMBO_ZRING=0)):
         c, old = _fresh_ctx(**knobs)
         try:
             outs.append(c.project(tau, "rotated", dims, (1, 1, 1)))
