@@ -245,7 +245,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   };
   p->xminb = knob("COMBO_XMINB", 2);
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
-  p->zpre = knob("COMBO_ZPRE", 1);
   p->zring = knob("COMBO_ZRING", 2);
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
@@ -1254,7 +1253,7 @@ int Solver::cg_solve(double tol_rel, double rr0, bool& breakdown, combo_host::St
           const double s = rr / pap;
           project_group(
               c_, cfg_.green, [&](size_t k) { return ProdLoad9{P(rb_, k), rk_[k].N}; },
-              [&](size_t k) { return ConsCgUpdate{P(r_, k), P(ap_, k), s, rk_[k].N, c_->plan->zpre}; }, 21);
+              [&](size_t k) { return ConsCgUpdate{P(r_, k), P(ap_, k), s, rk_[k].N}; }, 21);
           std::swap(r_, ap_);
         } else {
           project_group(

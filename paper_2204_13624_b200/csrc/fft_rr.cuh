@@ -316,21 +316,11 @@ __device__ __forceinline__ void zinv_finish(double2* sm, const double2* __restri
   [[maybe_unused]] double pre[2][8];
   if constexpr (Cons::PRELOAD) {
     if (active) {
-      if (cons.pre_mode == 2) {
-        // no registers: pull the lines into L1, the epilogue loads hit there
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = rr_final_pos<L, false>(u, i);
-          cons.touch(ca, cella + e);
-          if (hasb) cons.touch(cb, cellb + e);
-        }
-      } else if (cons.pre_mode == 1) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = rr_final_pos<L, false>(u, i);
-          pre[0][i] = cons.load(ca, cella + e);
-          pre[1][i] = hasb ? cons.load(cb, cellb + e) : 0.0;
-        }
+      for (int i = 0; i < 8; ++i) {
+        const int e = rr_final_pos<L, false>(u, i);
+        pre[0][i] = cons.load(ca, cella + e);
+        pre[1][i] = hasb ? cons.load(cb, cellb + e) : 0.0;
       }
     }
   }
@@ -346,13 +336,8 @@ __device__ __forceinline__ void zinv_finish(double2* sm, const double2* __restri
     for (int i = 0; i < 8; ++i) {
       const int e = rr_final_pos<L, false>(u, i);
       if constexpr (Cons::PRELOAD) {
-        if (cons.pre_mode == 1) {
-          pa += cons.comp_pre(ca, cella + e, v[0][i].x * scale, pre[0][i], sc);
-          if (hasb) pb += cons.comp_pre(cb, cellb + e, v[0][i].y * scale, pre[1][i], sc);
-        } else {
-          pa += cons.comp(ca, cella + e, v[0][i].x * scale, sc);
-          if (hasb) pb += cons.comp(cb, cellb + e, v[0][i].y * scale, sc);
-        }
+        pa += cons.comp_pre(ca, cella + e, v[0][i].x * scale, pre[0][i], sc);
+        if (hasb) pb += cons.comp_pre(cb, cellb + e, v[0][i].y * scale, pre[1][i], sc);
       } else {
         pa += cons.comp(ca, cella + e, v[0][i].x * scale, sc);
         if (hasb) pb += cons.comp(cb, cellb + e, v[0][i].y * scale, sc);

@@ -785,11 +785,7 @@ struct ConsCgUpdate {
   double* rnew;
   double step;
   int64_t N;
-  int pre_mode;  // r ahead of the inverse stages: 0 not, 1 into registers, 2 into L1 (prefetch)
   __device__ __forceinline__ double load(int c, int64_t cell) const { return r[c * N + cell]; }
-  __device__ __forceinline__ void touch(int c, int64_t cell) const {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c * N + cell));
-  }
   __device__ __forceinline__ double comp_pre(int c, int64_t cell, double v, double rold, double* sc) const {
     const double rn = rold - step * v;
     rnew[c * N + cell] = rn;
