@@ -110,7 +110,6 @@ struct FftPlan {
   bool mv_bulk = true;  // bulk-staged CG matvec (COMBO_MV_BULK=0: one cell per thread, direct loads)
   bool swap = false;  // j-major spectrum rows (see SpecView), COMBO_SWAP=1
   bool pq_dot = true;    // CG: pdir^T A pdir summed in the matvec (COMBO_PQ=0: in the z-inverse consumer)
-  int zpre = 1;          // z-inverse CG update at n3 = 512: r ahead of the stages into registers (1) or L1 (2)
   // TMA-staged column-strip passes (fft_tma.cuh): tensor maps over `spec`
   // (single slab, power-of-two axes); COMBO_XTMA / COMBO_YTMA = 0 turn them off
   // persistent ring-staged z-inverse at n3 = 512 (two consumer groups; COMBO_ZRING=0: one block per

@@ -245,7 +245,6 @@ void set_grid(combo_ctx* c, const int64_t* dims, const double* lengths) {
   };
   p->xminb = knob("COMBO_XMINB", 2);
   p->pq_dot = knob("COMBO_PQ", 1) != 0;
-  p->zpre = knob("COMBO_ZPRE", 1);
   p->zring = knob("COMBO_ZRING", 2);
   p->mv_bulk = knob("COMBO_MV_BULK", 1) != 0;
   p->split_sweep = knob("COMBO_SPLIT_SWEEP", 1) != 0;
@@ -597,18 +596,9 @@ int64_t launch_zinv(combo_ctx* c, const Cons& cons) {
       }
       if (ring) {
       } else {
-        auto go = [&](auto k) {
-          smem_attr(k, p.rzsmem);
-          k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
-        };
-        if constexpr (Cons::PRELOAD && L == 9) {
-          if (p.zpre == 2)
-            go(zinv_rr<Cons, L, 2>);
-          else
-            go(zinv_rr<Cons, L>);
-        } else {
-          go(zinv_rr<Cons, L>);
-        }
+        auto k = zinv_rr<Cons, L>;
+        smem_attr(k, p.rzsmem);
+        k<<<unsigned(nb), p.rzT, p.rzsmem, c->stream>>>(p.sv(), p.ax[2].tw.p, p.rzL, scale, cons, part);
       }
     } else {
       nb = (p.ni * p.dims[1] + p.zL - 1) / p.zL;

@@ -293,10 +293,7 @@ static __global__ void __launch_bounds__(512, 2)
 
 // Second half of a z-inverse tile: the completed natural-order pair lines
 // are in sm; inverse stages, then the consumer on the real outputs.
-// PRE selects how a PRELOAD consumer gets its field values ahead of the
-// stages: 1 into registers (spills at the 64-register cap), 2 by
-// prefetch.global.L1 (no registers; the epilogue loads then hit L1)
-template <class Cons, int L, class Sync = BlockSync, int PRE = 1>
+template <class Cons, int L, class Sync = BlockSync>
 __device__ __forceinline__ void zinv_finish(double2* sm, const double2* __restrict__ tw, int64_t line0, int nreal,
                                             int npair, double scale, const Cons& cons, double* partials,
                                             int64_t slot, int tid = threadIdx.x, int nthreads = blockDim.x,
@@ -322,13 +319,8 @@ __device__ __forceinline__ void zinv_finish(double2* sm, const double2* __restri
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int e = rr_final_pos<L, false>(u, i);
-        if constexpr (PRE == 2) {
-          cons.touch(ca, cella + e);
-          if (hasb) cons.touch(cb, cellb + e);
-        } else {
-          pre[0][i] = cons.load(ca, cella + e);
-          pre[1][i] = hasb ? cons.load(cb, cellb + e) : 0.0;
-        }
+        pre[0][i] = cons.load(ca, cella + e);
+        pre[1][i] = hasb ? cons.load(cb, cellb + e) : 0.0;
       }
     }
   }
@@ -343,7 +335,7 @@ __device__ __forceinline__ void zinv_finish(double2* sm, const double2* __restri
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int e = rr_final_pos<L, false>(u, i);
-      if constexpr (Cons::PRELOAD && PRE != 2) {
+      if constexpr (Cons::PRELOAD) {
         pa += cons.comp_pre(ca, cella + e, v[0][i].x * scale, pre[0][i], sc);
         if (hasb) pb += cons.comp_pre(cb, cellb + e, v[0][i].y * scale, pre[1][i], sc);
       } else {
@@ -363,7 +355,7 @@ __device__ __forceinline__ void zinv_finish(double2* sm, const double2* __restri
 // CG: spectrum loads bypass L1 (the fused Y/Z kernel reads rows other SMs
 // just wrote); DISCARD: the consumed spectrum rows are dropped from L2
 // without write-back (dead after this pass).
-template <class Cons, int L, bool CG = false, bool DISCARD = false, int PRE = 1>
+template <class Cons, int L, bool CG = false, bool DISCARD = false>
 __device__ __forceinline__ void zinv_tile(const SpecView& sv, const double2* __restrict__ tw, int64_t line0,
                                           int nlines, double scale, const Cons& cons, double* partials,
                                           int64_t slot, bool discard = true) {
@@ -428,16 +420,16 @@ __device__ __forceinline__ void zinv_tile(const SpecView& sv, const double2* __r
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
     }
   }
-  zinv_finish<Cons, L, BlockSync, PRE>(sm, tw, line0, nreal, npair, scale, cons, partials, slot);
+  zinv_finish<Cons, L>(sm, tw, line0, nreal, npair, scale, cons, partials, slot);
 }
 
-template <class Cons, int L, int PRE = 1>
+template <class Cons, int L>
 static __global__ void __launch_bounds__(512, 2)
     zinv_rr(SpecView sv, const double2* __restrict__ tw, int nl_per_block, double scale, Cons cons,
             double* partials) {
   const int64_t nlines_tot = sv.ni * sv.n2;  // local z-lines
   const int64_t line0 = int64_t(blockIdx.x) * nl_per_block;
-  zinv_tile<Cons, L, false, false, PRE>(sv, tw, line0, int(min(int64_t(nl_per_block), nlines_tot - line0)), scale, cons, partials,
+  zinv_tile<Cons, L>(sv, tw, line0, int(min(int64_t(nl_per_block), nlines_tot - line0)), scale, cons, partials,
                      blockIdx.x);
 }
 

@@ -786,9 +786,6 @@ struct ConsCgUpdate {
   double step;
   int64_t N;
   __device__ __forceinline__ double load(int c, int64_t cell) const { return r[c * N + cell]; }
-  __device__ __forceinline__ void touch(int c, int64_t cell) const {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c * N + cell));
-  }
   __device__ __forceinline__ double comp_pre(int c, int64_t cell, double v, double rold, double* sc) const {
     const double rn = rold - step * v;
     rnew[c * N + cell] = rn;
